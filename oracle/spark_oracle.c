@@ -1,0 +1,537 @@
+/*
+ * spark_oracle.c — CPU oracle for the Spark block-update hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_2401_03378_b200/, libspark) never links, imports
+ * or calls it, and this file shares no code, header or constant with it.
+ *
+ * Plain, slow, obviously-correct FP64 C.  Build: gcc -O2 -ffp-contract=off
+ * -fno-fast-math -fopenmp (no FMA contraction, no reassociation).
+ *
+ * What it computes, in the paper's order (PAPER.md = /root/reference/PAPER.md):
+ *   - lst:spark-nontelescoping: for every RK stage, first
+ *     fill_guardcells() for all blocks, then for every block the block
+ *     initialisation (Alg. 7: initSoln keeps U^n) and the
+ *     intra-stage calculations (Alg. 8):
+ *     grvAccel (identity, no gravity) -> calcLims (reconstruction) ->
+ *     calcFlux (Riemann) -> updSoln (divergence + RK combination) ->
+ *     calcEos (pressure / positivity check).  fluxBuff is not needed on a
+ *     single-level grid (no coarse-fine faces).
+ *   - Blocks have identical cell counts and a surrounding halo of guard
+ *     cells that makes each block look like a whole domain:
+ *     this oracle materialises exactly that padded per-block array.
+ *   - SSP-RK time stepping (Gottlieb & Shu 1998).
+ * The paper states no formulas for the numerics; every formula below is the
+ * textbook reading recorded in DESIGN.md §3:
+ *   ideal-gas EOS; PLM-minmod / WENO5-JS on primitive variables with a
+ *   first-order positivity fallback; HLL / HLLC (Toro §10.4) with Davis wave
+ *   speeds; CFL dt = C min_cells min_d dx_d/(|u_d|+c); Shu-Osher SSP-RK2/3.
+ *
+ * Layouts (identical meaning to include/spark.h, defined here independently):
+ *   canonical  U[v][b][k][j][i]            fp64, i fastest, b lexicographic
+ *   padded     P[v][b][k+gz][j+gy][i+gx]   gd = ng for d < ndim, else 0
+ * Variables: v = 0 rho, 1..ndim momentum, ndim+1 total energy.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+    int32_t ndim;
+    int32_t nb[3];
+    int32_t nblk[3];
+    int32_t ng;
+    double lo[3], hi[3];
+    int32_t bc[3][2];       /* 0 periodic, 1 outflow, 2 reflect */
+    int32_t recon;          /* 0 first order, 1 PLM-minmod, 2 WENO5-JS */
+    int32_t riemann;        /* 0 HLL, 1 HLLC */
+    int32_t rk_stages;      /* 2 or 3 */
+    double gamma, cfl;
+} ocfg;
+
+enum { OBC_PERIODIC = 0, OBC_OUTFLOW = 1, OBC_REFLECT = 2 };
+enum { OREC_FIRST = 0, OREC_PLM = 1, OREC_WENO5 = 2 };
+enum { ORS_HLL = 0, ORS_HLLC = 1 };
+
+/* status codes */
+enum { OK = 0, OERR_ARG = 1, OERR_NONPHYSICAL = 5, OERR_OOM = 4 };
+
+/* ---------------------------------------------------------------- geometry */
+static int nvar_of(const ocfg* c) { return c->ndim + 2; }
+static long cells_per_block(const ocfg* c) { return (long)c->nb[0] * c->nb[1] * c->nb[2]; }
+static long nblocks(const ocfg* c) { return (long)c->nblk[0] * c->nblk[1] * c->nblk[2]; }
+static int guard_of(const ocfg* c, int d) { return d < c->ndim ? c->ng : 0; }
+static long padded_cells(const ocfg* c) {
+    long n = 1;
+    for (int d = 0; d < 3; d++) n *= c->nb[d] + 2 * guard_of(c, d);
+    return n;
+}
+static double dx_of(const ocfg* c, int d) {
+    return (c->hi[d] - c->lo[d]) / ((double)c->nblk[d] * (double)c->nb[d]);
+}
+
+int oracle_check_config(const ocfg* c) {
+    if (c->ndim < 1 || c->ndim > 3) return OERR_ARG;
+    for (int d = 0; d < 3; d++) {
+        if (c->nb[d] < 1 || c->nblk[d] < 1) return OERR_ARG;
+        if (d >= c->ndim && (c->nb[d] != 1 || c->nblk[d] != 1)) return OERR_ARG;
+        if (d < c->ndim && c->nb[d] < c->ng) return OERR_ARG;
+    }
+    int need = c->recon == OREC_WENO5 ? 3 : (c->recon == OREC_PLM ? 2 : 1);
+    if (c->recon < 0 || c->recon > 2 || c->ng < need) return OERR_ARG;
+    if (c->riemann < 0 || c->riemann > 1) return OERR_ARG;
+    if (c->rk_stages != 2 && c->rk_stages != 3) return OERR_ARG;
+    if (!(c->gamma > 1.0) || !(c->cfl > 0.0)) return OERR_ARG;
+    return OK;
+}
+
+/* Guard-cell map along one dimension (reading R4): global cell
+ * index g (possibly outside [0,N)) -> interior index; *flip = 1 when a
+ * reflecting wall mirrors the cell (normal momentum changes sign). */
+static long map_dim(long g, long N, int bc_lo, int bc_hi, int* flip) {
+    *flip = 0;
+    if (g >= 0 && g < N) return g;
+    int bc = g < 0 ? bc_lo : bc_hi;
+    if (bc == OBC_PERIODIC) {
+        long m = g % N;
+        if (m < 0) m += N;
+        return m;
+    }
+    if (bc == OBC_OUTFLOW) return g < 0 ? 0 : N - 1;
+    *flip = 1; /* reflect */
+    return g < 0 ? -1 - g : 2 * N - 1 - g;
+}
+
+/* fill_guardcells: padded per-block copy of U with
+ * every guard cell (faces, edges, corners) taken from the per-dimension map
+ * of its global index.  Interior cells are copied unchanged. */
+int oracle_fill_guardcells(const ocfg* c, const double* U, double* P) {
+    if (oracle_check_config(c)) return OERR_ARG;
+    const int nv = nvar_of(c);
+    const long NB = nblocks(c), nc = cells_per_block(c), np = padded_cells(c);
+    const long N[3] = {(long)c->nblk[0] * c->nb[0], (long)c->nblk[1] * c->nb[1],
+                       (long)c->nblk[2] * c->nb[2]};
+    const int g[3] = {guard_of(c, 0), guard_of(c, 1), guard_of(c, 2)};
+    const int pn[3] = {c->nb[0] + 2 * g[0], c->nb[1] + 2 * g[1], c->nb[2] + 2 * g[2]};
+#pragma omp parallel for schedule(static)
+    for (long b = 0; b < NB; b++) {
+        long bx = b % c->nblk[0], by = (b / c->nblk[0]) % c->nblk[1], bz = b / ((long)c->nblk[0] * c->nblk[1]);
+        for (int pk = 0; pk < pn[2]; pk++)
+            for (int pj = 0; pj < pn[1]; pj++)
+                for (int pi = 0; pi < pn[0]; pi++) {
+                    int fx, fy, fz;
+                    long gx = map_dim(bx * c->nb[0] + pi - g[0], N[0], c->bc[0][0], c->bc[0][1], &fx);
+                    long gy = map_dim(by * c->nb[1] + pj - g[1], N[1], c->bc[1][0], c->bc[1][1], &fy);
+                    long gz = map_dim(bz * c->nb[2] + pk - g[2], N[2], c->bc[2][0], c->bc[2][1], &fz);
+                    long sb = (gx / c->nb[0]) + c->nblk[0] * ((gy / c->nb[1]) + c->nblk[1] * (gz / c->nb[2]));
+                    long sc = ((gz % c->nb[2]) * c->nb[1] + (gy % c->nb[1])) * c->nb[0] + (gx % c->nb[0]);
+                    long pidx = ((long)pk * pn[1] + pj) * pn[0] + pi;
+                    int flip[3] = {fx, fy, fz};
+                    for (int v = 0; v < nv; v++) {
+                        double val = U[(long)v * NB * nc + sb * nc + sc];
+                        if (v >= 1 && v <= c->ndim && flip[v - 1]) val = -val;
+                        P[(long)v * NB * np + b * np + pidx] = val;
+                    }
+                }
+    }
+    return OK;
+}
+
+/* ------------------------------------------------------------------- EOS */
+/* EOS unit, ideal gas: p = (gamma-1)(E - 1/2 |m|^2/rho). */
+static void cons_to_prim(int ndim, double gamma, const double* u, double* w) {
+    double rho = u[0];
+    double ke = 0.0;
+    for (int d = 0; d < ndim; d++) ke += u[1 + d] * u[1 + d];
+    w[0] = rho;
+    for (int d = 0; d < ndim; d++) w[1 + d] = u[1 + d] / rho;
+    w[ndim + 1] = (gamma - 1.0) * (u[ndim + 1] - 0.5 * ke / rho);
+}
+
+/* E = p/(gamma-1) + 1/2 rho |u|^2. */
+static void prim_to_cons(int ndim, double gamma, const double* w, double* u) {
+    double rho = w[0];
+    double u2 = 0.0;
+    for (int d = 0; d < ndim; d++) u2 += w[1 + d] * w[1 + d];
+    u[0] = rho;
+    for (int d = 0; d < ndim; d++) u[1 + d] = rho * w[1 + d];
+    u[ndim + 1] = w[ndim + 1] / (gamma - 1.0) + 0.5 * rho * u2;
+}
+
+/* Canonical-layout conversions over ncells cells (arrays [nvar][ncells]). */
+void oracle_prim_to_cons(int ndim, double gamma, long ncells, const double* W, double* U) {
+    int nv = ndim + 2;
+    for (long n = 0; n < ncells; n++) {
+        double w[5], u[5];
+        for (int v = 0; v < nv; v++) w[v] = W[(long)v * ncells + n];
+        prim_to_cons(ndim, gamma, w, u);
+        for (int v = 0; v < nv; v++) U[(long)v * ncells + n] = u[v];
+    }
+}
+
+void oracle_cons_to_prim(int ndim, double gamma, long ncells, const double* U, double* W) {
+    int nv = ndim + 2;
+    for (long n = 0; n < ncells; n++) {
+        double w[5], u[5];
+        for (int v = 0; v < nv; v++) u[v] = U[(long)v * ncells + n];
+        cons_to_prim(ndim, gamma, u, w);
+        for (int v = 0; v < nv; v++) W[(long)v * ncells + n] = w[v];
+    }
+}
+
+/* --------------------------------------------------------- reconstruction */
+/* calcLims.  minmod (reading R2): 0 unless a and b are
+ * both strictly positive or both strictly negative; then the one of
+ * smaller magnitude. */
+static double minmod(double a, double b) {
+    if (a > 0.0 && b > 0.0) return a < b ? a : b;
+    if (a < 0.0 && b < 0.0) return a > b ? a : b;
+    return 0.0;
+}
+
+/* PLM face states at i+1/2 from W_{i-1}, W_i, W_{i+1}, W_{i+2}. */
+void oracle_plm_face(double wm1, double w0, double w1, double w2, double* wl, double* wr) {
+    double d0 = minmod(w0 - wm1, w1 - w0);
+    double d1 = minmod(w1 - w0, w2 - w1);
+    *wl = w0 + 0.5 * d0;
+    *wr = w1 - 0.5 * d1;
+}
+
+/* WENO5-JS (Jiang & Shu 1996) value at the right edge of cell c from the
+ * cell averages (a,b,c,d,e) = W_{i-2..i+2}: DESIGN.md reading R3. */
+double oracle_weno5_edge(double a, double b, double c, double d, double e) {
+    const double eps = 1e-6;
+    double b0 = 13.0 / 12.0 * (a - 2.0 * b + c) * (a - 2.0 * b + c) + 0.25 * (a - 4.0 * b + 3.0 * c) * (a - 4.0 * b + 3.0 * c);
+    double b1 = 13.0 / 12.0 * (b - 2.0 * c + d) * (b - 2.0 * c + d) + 0.25 * (b - d) * (b - d);
+    double b2 = 13.0 / 12.0 * (c - 2.0 * d + e) * (c - 2.0 * d + e) + 0.25 * (3.0 * c - 4.0 * d + e) * (3.0 * c - 4.0 * d + e);
+    double a0 = 0.1 / ((eps + b0) * (eps + b0));
+    double a1 = 0.6 / ((eps + b1) * (eps + b1));
+    double a2 = 0.3 / ((eps + b2) * (eps + b2));
+    double q0 = (2.0 * a - 7.0 * b + 11.0 * c) / 6.0;
+    double q1 = (-b + 5.0 * c + 2.0 * d) / 6.0;
+    double q2 = (2.0 * c + 5.0 * d - e) / 6.0;
+    return (a0 * q0 + a1 * q1 + a2 * q2) / (a0 + a1 + a2);
+}
+
+/* WENO5 face states at i+1/2 from W_{i-2..i+3} (s[0..5]). */
+void oracle_weno5_face(const double* s, double* wl, double* wr) {
+    *wl = oracle_weno5_edge(s[0], s[1], s[2], s[3], s[4]);
+    *wr = oracle_weno5_edge(s[5], s[4], s[3], s[2], s[1]);
+}
+
+/* Face states for all nvar primitive components.  st[m*nv + v] holds the
+ * stencil W_{i-ng+1+m} (m = 0..2ng-1) for a face at i+1/2.  Components are in
+ * the rotated frame (rho, u_n, u_t..., p).  Positivity fallback: first order
+ * when rho or p of either state is <= 0. */
+static void reconstruct(int recon, int ng, int nv, const double* st, double* wl, double* wr) {
+    const double* c0 = st + (ng - 1) * nv; /* W_i   */
+    const double* c1 = st + ng * nv;       /* W_i+1 */
+    for (int v = 0; v < nv; v++) {
+        if (recon == OREC_FIRST) {
+            wl[v] = c0[v];
+            wr[v] = c1[v];
+        } else if (recon == OREC_PLM) {
+            oracle_plm_face(st[(ng - 2) * nv + v], c0[v], c1[v], st[(ng + 1) * nv + v], &wl[v], &wr[v]);
+        } else {
+            double s[6];
+            for (int m = 0; m < 6; m++) s[m] = st[(ng - 3 + m) * nv + v];
+            oracle_weno5_face(s, &wl[v], &wr[v]);
+        }
+    }
+    if (!(wl[0] > 0.0) || !(wl[nv - 1] > 0.0) || !(wr[0] > 0.0) || !(wr[nv - 1] > 0.0)) {
+        for (int v = 0; v < nv; v++) {
+            wl[v] = c0[v];
+            wr[v] = c1[v];
+        }
+    }
+}
+
+/* ------------------------------------------------------------------ Riemann */
+/* Physical flux along the normal of the rotated frame (rho, u_n, u_t.., p).
+ * ax[e] is the rotated index of axis e: |u|^2 is summed in axis order
+ * (u_x^2 + u_y^2) + u_z^2 whatever the direction (reading R9). */
+static void phys_flux(int nv, double gamma, const int* ax, const double* w, double* u, double* f) {
+    double rho = w[0], un = w[1], p = w[nv - 1];
+    double u2 = 0.0;
+    for (int e = 0; e < nv - 2; e++) u2 += w[ax[e]] * w[ax[e]];
+    u[0] = rho;
+    for (int m = 1; m < nv - 1; m++) u[m] = rho * w[m];
+    u[nv - 1] = p / (gamma - 1.0) + 0.5 * rho * u2;
+    f[0] = rho * un;
+    f[1] = rho * un * un + p;
+    for (int m = 2; m < nv - 1; m++) f[m] = rho * un * w[m];
+    f[nv - 1] = un * (u[nv - 1] + p);
+}
+
+/* calcFlux: HLL or HLLC (Toro §10.4) with Davis wave speeds
+ * (readings R5, R6).  wl, wr, f are in the rotated frame. */
+static void riemann_ax(int riemann, int nv, double gamma, const int* ax, const double* wl, const double* wr,
+                       double* f) {
+    double ul[5], ur[5], fl[5], fr[5];
+    phys_flux(nv, gamma, ax, wl, ul, fl);
+    phys_flux(nv, gamma, ax, wr, ur, fr);
+    double rl = wl[0], uL = wl[1], pl = wl[nv - 1];
+    double rr = wr[0], uR = wr[1], pr = wr[nv - 1];
+    double cl = sqrt(gamma * pl / rl), cr = sqrt(gamma * pr / rr);
+    double sl = fmin(uL - cl, uR - cr);
+    double sr = fmax(uL + cl, uR + cr);
+    if (sl >= 0.0) {
+        for (int v = 0; v < nv; v++) f[v] = fl[v];
+        return;
+    }
+    if (sr <= 0.0) {
+        for (int v = 0; v < nv; v++) f[v] = fr[v];
+        return;
+    }
+    if (riemann == ORS_HLL) {
+        for (int v = 0; v < nv; v++)
+            f[v] = (sr * fl[v] - sl * fr[v] + sl * sr * (ur[v] - ul[v])) / (sr - sl);
+        return;
+    }
+    double sstar = (pr - pl + rl * uL * (sl - uL) - rr * uR * (sr - uR)) / (rl * (sl - uL) - rr * (sr - uR));
+    const double* w = sstar >= 0.0 ? wl : wr;
+    const double* uk = sstar >= 0.0 ? ul : ur;
+    const double* fk = sstar >= 0.0 ? fl : fr;
+    double sk = sstar >= 0.0 ? sl : sr;
+    double rho = w[0], un = w[1], p = w[nv - 1];
+    double fac = rho * (sk - un) / (sk - sstar);
+    double us[5];
+    us[0] = fac;
+    us[1] = fac * sstar;
+    for (int m = 2; m < nv - 1; m++) us[m] = fac * w[m];
+    us[nv - 1] = fac * (uk[nv - 1] / rho + (sstar - un) * (sstar + p / (rho * (sk - un))));
+    for (int v = 0; v < nv; v++) f[v] = fk[v] + sk * (us[v] - uk[v]);
+}
+
+/* Public entry for the pins: states already in the frame whose normal is
+ * axis 0 (identity rotation). */
+void oracle_riemann(int riemann, int nv, double gamma, const double* wl, const double* wr, double* f) {
+    int ax[3] = {1, 2, 3};
+    riemann_ax(riemann, nv, gamma, ax, wl, wr, f);
+}
+
+/* Rotation for direction d (reading R9): rotated components
+ * (rho, u_d, the other velocities in increasing axis order, p).  rot[m] is
+ * the unrotated component index of rotated component m. */
+static void rotation(int ndim, int d, int* rot, int* ax) {
+    int nv = ndim + 2, m = 2;
+    rot[0] = 0;
+    rot[1] = 1 + d;
+    ax[d] = 1;
+    for (int e = 0; e < ndim; e++)
+        if (e != d) { ax[e] = m; rot[m++] = 1 + e; }
+    rot[nv - 1] = nv - 1;
+}
+
+/* ------------------------------------------------------------- dt (CFL) */
+/* dt = C * min_cells min_d dx_d/(|u_d| + c)  (reading R7). */
+double oracle_dt_raw(const ocfg* c, const double* U) {
+    const int nv = nvar_of(c);
+    const long n = nblocks(c) * cells_per_block(c);
+    double dx[3] = {dx_of(c, 0), dx_of(c, 1), dx_of(c, 2)};
+    double best = INFINITY;
+    for (long q = 0; q < n; q++) {
+        double u[5], w[5];
+        for (int v = 0; v < nv; v++) u[v] = U[(long)v * n + q];
+        cons_to_prim(c->ndim, c->gamma, u, w);
+        double cs = sqrt(c->gamma * w[nv - 1] / w[0]);
+        for (int d = 0; d < c->ndim; d++) {
+            double t = dx[d] / (fabs(w[1 + d]) + cs);
+            if (t < best) best = t;
+        }
+    }
+    return best;
+}
+
+double oracle_dt(const ocfg* c, const double* U, double t, double t_end) {
+    double dt = c->cfl * oracle_dt_raw(c, U);
+    if (t_end > 0.0 && dt > t_end - t) dt = t_end - t;
+    return dt;
+}
+
+/* ------------------------------------------------------------ one stage */
+/* Intra-stage calculations (Alg. 8) on every block of an
+ * already-filled padded array P (U^(s-1) with guards):
+ *   U_out = a * Un + b * (U_prev + dt * L(U_prev))
+ * with L = -[(Fx+ - Fx-)/dx + (Fy+ - Fy-)/dy] - (Fz+ - Fz-)/dz (reading R8).
+ * U_prev is read from the interior of P.  Un may be NULL when a == 0.
+ * Returns OERR_NONPHYSICAL if any updated cell has rho <= 0, p <= 0 or a
+ * non-finite value (calcEos; reading R12). */
+int oracle_stage_padded(const ocfg* c, const double* P, const double* Un, double a, double b, double dt,
+                        double* Uout) {
+    if (oracle_check_config(c)) return OERR_ARG;
+    const int nv = nvar_of(c), ng = c->ng, ndim = c->ndim;
+    const long NB = nblocks(c), nc = cells_per_block(c), np = padded_cells(c);
+    const int g[3] = {guard_of(c, 0), guard_of(c, 1), guard_of(c, 2)};
+    const int pn[3] = {c->nb[0] + 2 * g[0], c->nb[1] + 2 * g[1], c->nb[2] + 2 * g[2]};
+    const long pstride[3] = {1, pn[0], (long)pn[0] * pn[1]};
+    double dx[3] = {dx_of(c, 0), dx_of(c, 1), dx_of(c, 2)};
+    int bad = 0;
+#pragma omp parallel reduction(| : bad)
+    {
+        double* W = malloc(sizeof(double) * nv * np);          /* primitives on the padded tile */
+        double* F[3] = {NULL, NULL, NULL};                     /* face fluxes per direction */
+        long nf[3] = {0, 0, 0};
+        for (int d = 0; d < ndim; d++) {
+            nf[d] = 1;
+            for (int e = 0; e < 3; e++) nf[d] *= c->nb[e] + (e == d ? 1 : 0);
+            F[d] = malloc(sizeof(double) * nv * nf[d]);
+        }
+#pragma omp for schedule(static)
+        for (long blk = 0; blk < NB; blk++) {
+            const double* Pb = P + blk * np;
+            /* block init: primitives from the EOS on every padded cell */
+            for (long q = 0; q < np; q++) {
+                double u[5], w[5];
+                for (int v = 0; v < nv; v++) u[v] = Pb[(long)v * NB * np + q];
+                cons_to_prim(ndim, c->gamma, u, w);
+                for (int v = 0; v < nv; v++) W[(long)v * np + q] = w[v];
+            }
+            /* calcLims + calcFlux per direction */
+            for (int d = 0; d < ndim; d++) {
+                int rot[5], ax[3];
+                rotation(ndim, d, rot, ax);
+                int fn[3] = {c->nb[0], c->nb[1], c->nb[2]};
+                fn[d] += 1;
+                for (int k = 0; k < fn[2]; k++)
+                    for (int j = 0; j < fn[1]; j++)
+                        for (int i = 0; i < fn[0]; i++) {
+                            /* face between cells (idx-1) and idx along d; padded coords
+                             * of the cell on its right are (i,j,k)+g. */
+                            long right = ((long)(k + g[2]) * pn[1] + (j + g[1])) * pn[0] + (i + g[0]);
+                            double st[6 * 5], wl[5], wr[5], fr[5];
+                            for (int m = 0; m < 2 * ng; m++) {
+                                long q = right + (long)(m - ng) * pstride[d];
+                                for (int v = 0; v < nv; v++) st[m * nv + v] = W[(long)rot[v] * np + q];
+                            }
+                            reconstruct(c->recon, ng, nv, st, wl, wr);
+                            riemann_ax(c->riemann, nv, c->gamma, ax, wl, wr, fr);
+                            long fidx = ((long)k * fn[1] + j) * fn[0] + i;
+                            for (int v = 0; v < nv; v++) F[d][(long)rot[v] * nf[d] + fidx] = fr[v];
+                        }
+            }
+            /* updSoln + calcEos */
+            for (int k = 0; k < c->nb[2]; k++)
+                for (int j = 0; j < c->nb[1]; j++)
+                    for (int i = 0; i < c->nb[0]; i++) {
+                        long cell = ((long)k * c->nb[1] + j) * c->nb[0] + i;
+                        long pcell = ((long)(k + g[2]) * pn[1] + (j + g[1])) * pn[0] + (i + g[0]);
+                        double unew[5];
+                        for (int v = 0; v < nv; v++) {
+                            double div[3] = {0.0, 0.0, 0.0};
+                            for (int d = 0; d < ndim; d++) {
+                                int fn[3] = {c->nb[0], c->nb[1], c->nb[2]};
+                                fn[d] += 1;
+                                int lo[3] = {i, j, k};
+                                int hi[3] = {i, j, k};
+                                hi[d] += 1;
+                                long flo = ((long)lo[2] * fn[1] + lo[1]) * fn[0] + lo[0];
+                                long fhi = ((long)hi[2] * fn[1] + hi[1]) * fn[0] + hi[0];
+                                div[d] = (F[d][(long)v * nf[d] + fhi] - F[d][(long)v * nf[d] + flo]) / dx[d];
+                            }
+                            double L;
+                            if (ndim == 1) L = -(div[0]);
+                            else if (ndim == 2) L = -(div[0] + div[1]);
+                            else L = -(div[0] + div[1]) - div[2];
+                            double uprev = Pb[(long)v * NB * np + pcell];
+                            double un = Un ? Un[(long)v * NB * nc + blk * nc + cell] : 0.0;
+                            double val = a * un + b * (uprev + dt * L);
+                            unew[v] = val;
+                            Uout[(long)v * NB * nc + blk * nc + cell] = val;
+                        }
+                        double w[5];
+                        cons_to_prim(ndim, c->gamma, unew, w);
+                        int ok = w[0] > 0.0 && w[nv - 1] > 0.0;
+                        for (int v = 0; v < nv; v++) ok = ok && isfinite(unew[v]);
+                        if (!ok) bad = 1;
+                    }
+        }
+        free(W);
+        for (int d = 0; d < 3; d++) free(F[d]);
+    }
+    return bad ? OERR_NONPHYSICAL : OK;
+}
+
+/* RK coefficients (Shu-Osher form, reading R10): stage s (1-based) computes
+ * U^(s) = a_s U^n + b_s (U^(s-1) + dt L(U^(s-1))). */
+void oracle_rk_coeffs(int stages, int s, double* a, double* b) {
+    if (stages == 2) {
+        if (s == 1) { *a = 0.0; *b = 1.0; }
+        else { *a = 0.5; *b = 0.5; }
+    } else {
+        if (s == 1) { *a = 0.0; *b = 1.0; }
+        else if (s == 2) { *a = 0.75; *b = 0.25; }
+        else { *a = 1.0 / 3.0; *b = 2.0 / 3.0; }
+    }
+}
+
+/* One stage from the canonical layout: fill_guardcells then the block loop
+ * (lst:spark-nontelescoping body). */
+int oracle_stage(const ocfg* c, const double* Uprev, const double* Un, double a, double b, double dt,
+                 double* Uout) {
+    if (oracle_check_config(c)) return OERR_ARG;
+    size_t bytes = sizeof(double) * nvar_of(c) * nblocks(c) * padded_cells(c);
+    double* P = malloc(bytes);
+    if (!P) return OERR_OOM;
+    oracle_fill_guardcells(c, Uprev, P);
+    int st = oracle_stage_padded(c, P, Un, a, b, dt, Uout);
+    free(P);
+    return st;
+}
+
+/* One SSP-RK step in place on U (lst:spark-nontelescoping).
+ * dt_fixed > 0 uses that dt; otherwise the CFL dt of U^n clipped to t_end - t
+ * (t_end <= 0: no clip).  *dt_used receives the dt.  On a non-physical stage
+ * U is left unchanged (U^n retained) and OERR_NONPHYSICAL is returned. */
+int oracle_step(const ocfg* c, double* U, double t, double t_end, double dt_fixed, double* dt_used) {
+    if (oracle_check_config(c)) return OERR_ARG;
+    size_t n = (size_t)nvar_of(c) * nblocks(c) * cells_per_block(c);
+    double dt = dt_fixed > 0.0 ? dt_fixed : oracle_dt(c, U, t, t_end);
+    if (dt_used) *dt_used = dt;
+    double* S0 = malloc(sizeof(double) * n);
+    double* S1 = malloc(sizeof(double) * n);
+    if (!S0 || !S1) { free(S0); free(S1); return OERR_OOM; }
+    const double* prev = U;
+    double* bufs[2] = {S0, S1};
+    int st = OK;
+    for (int s = 1; s <= c->rk_stages && st == OK; s++) {
+        double a, b;
+        oracle_rk_coeffs(c->rk_stages, s, &a, &b);
+        double* out = bufs[(s - 1) & 1];
+        st = oracle_stage(c, prev, U, a, b, dt, out);
+        prev = out;
+    }
+    if (st == OK) memcpy(U, prev, sizeof(double) * n);
+    free(S0);
+    free(S1);
+    return st;
+}
+
+/* Run to t_end (t_end > 0) and/or for at most max_steps steps (>0).
+ * Stop rule (reading R8): t >= t_end * (1 - 1e-14).  Returns status; *t and
+ * *nsteps are updated. */
+int oracle_run(const ocfg* c, double* U, double t_end, long max_steps, double* t, long* nsteps) {
+    int st = OK;
+    while (st == OK) {
+        if (t_end > 0.0 && *t >= t_end * (1.0 - 1e-14)) break;
+        if (max_steps > 0 && *nsteps >= max_steps) break;
+        double dt;
+        st = oracle_step(c, U, *t, t_end, 0.0, &dt);
+        if (st == OK) {
+            *t += dt;
+            *nsteps += 1;
+        }
+    }
+    return st;
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+    extern int omp_get_max_threads(void);
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -1,0 +1,251 @@
+"""Seeded synthetic input generators shared by the oracle tests and the CUDA path.
+
+This module holds NO arithmetic of the method (no EOS, reconstruction, Riemann
+solver, divergence or RK).  It only produces:
+
+* problem descriptions (``PRESETS``: the five BASELINE.json configs),
+* primitive initial states ``W[v][b][k][j][i]`` (rho, u_1..u_ndim, p) — each side
+  converts them to conserved variables with its own EOS,
+* index permutations between the canonical block layout and a global
+  ``[v][z][y][x]`` array (pure reshapes),
+* seeded random states (numpy ``Generator(PCG64(seed))``).
+
+Input recipes:
+  Sod    (rho,u,p) = (1,0,1) for x < 0.5, (0.125,0,0.1) otherwise  [Toro 2009 Test 1]
+  Sedov  rho = 1, u = 0, p_amb = 1e-5; E_blast = 1 deposited uniformly as
+         internal energy in the cells whose centres lie within r0 = 3.5 dx of
+         the domain centre
+  random rho, p ~ U[0.5, 1.5], u_d ~ U[-0.5, 0.5]; "blocky" adds jumps of
+         rho x10 and p x100 every 5-13 cells along x (limiter branches)
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+BC_PERIODIC, BC_OUTFLOW, BC_REFLECT = 0, 1, 2
+RECON_FIRST, RECON_PLM, RECON_WENO5 = 0, 1, 2
+RIEMANN_HLL, RIEMANN_HLLC = 0, 1
+
+
+@dataclass(frozen=True)
+class Problem:
+    """A problem description: the fields of spark_config plus the IC name."""
+
+    name: str
+    ndim: int
+    nb: tuple
+    nblk: tuple
+    ng: int
+    recon: int
+    riemann: int
+    rk_stages: int
+    cfl: float
+    bc: tuple = ((BC_OUTFLOW, BC_OUTFLOW),) * 3
+    lo: tuple = (0.0, 0.0, 0.0)
+    hi: tuple = (1.0, 1.0, 1.0)
+    gamma: float = 1.4
+    ic: str = "sod"
+    t_end: float = 0.0
+
+    def config(self) -> dict:
+        return dict(ndim=self.ndim, nb=tuple(self.nb), nblk=tuple(self.nblk), ng=self.ng, lo=tuple(self.lo),
+                    hi=tuple(self.hi), bc=tuple(tuple(x) for x in self.bc), recon=self.recon,
+                    riemann=self.riemann, rk_stages=self.rk_stages, gamma=self.gamma, cfl=self.cfl)
+
+    def with_(self, **kw) -> "Problem":
+        return replace(self, **kw)
+
+    @property
+    def nvar(self):
+        return self.ndim + 2
+
+    @property
+    def ncells(self):
+        return int(np.prod(self.nb)) * int(np.prod(self.nblk))
+
+
+_OUT = ((BC_OUTFLOW, BC_OUTFLOW),) * 3
+_PER = ((BC_PERIODIC, BC_PERIODIC),) * 3
+
+# The five BASELINE.json configs.
+PRESETS = {
+    # configs[0]: 1-D Sod, 256 cells = 32 blocks x 8, RK2 + PLM + HLLC, t = 0.2
+    "c1_sod1d": Problem("c1_sod1d", 1, (8, 1, 1), (32, 1, 1), 2, RECON_PLM, RIEMANN_HLLC, 2, 0.8,
+                        bc=_OUT, ic="sod_x", t_end=0.2),
+    # configs[1] reading C2a: x-aligned Sod, outflow in x, periodic in y
+    "c2a_sod2d": Problem("c2a_sod2d", 2, (16, 16, 1), (8, 8, 1), 2, RECON_PLM, RIEMANN_HLLC, 2, 0.4,
+                         bc=((BC_OUTFLOW, BC_OUTFLOW), (BC_PERIODIC, BC_PERIODIC), (BC_OUTFLOW, BC_OUTFLOW)),
+                         ic="sod_x", t_end=0.2),
+    # configs[1] reading C2b: fully periodic square Sod (conservation)
+    "c2b_sod2d": Problem("c2b_sod2d", 2, (16, 16, 1), (8, 8, 1), 2, RECON_PLM, RIEMANN_HLLC, 2, 0.4,
+                         bc=_PER, ic="sod_square", t_end=0.1),
+    # configs[2]: 2-D Sedov 1024^2 in 16^2 blocks, RK3 + WENO5 + HLLC
+    "c3_sedov2d": Problem("c3_sedov2d", 2, (16, 16, 1), (64, 64, 1), 3, RECON_WENO5, RIEMANN_HLLC, 3, 0.4,
+                          bc=_OUT, ic="sedov", t_end=0.05),
+    # configs[3]: 3-D Sedov 256^3 in 16^3 blocks (PLM/RK2 and WENO5/RK3 variants)
+    "c4_sedov3d_plm": Problem("c4_sedov3d_plm", 3, (16, 16, 16), (16, 16, 16), 2, RECON_PLM, RIEMANN_HLLC, 2,
+                              0.3, bc=_OUT, ic="sedov", t_end=0.05),
+    "c4_sedov3d_weno": Problem("c4_sedov3d_weno", 3, (16, 16, 16), (16, 16, 16), 3, RECON_WENO5, RIEMANN_HLLC,
+                               3, 0.3, bc=_OUT, ic="sedov", t_end=0.05),
+    # configs[4]: 3-D Sedov 1024^3 in 16^3 blocks over 2/4/8 GPUs
+    "c5_sedov3d_plm": Problem("c5_sedov3d_plm", 3, (16, 16, 16), (64, 64, 64), 2, RECON_PLM, RIEMANN_HLLC, 2,
+                              0.3, bc=_OUT, ic="sedov", t_end=0.05),
+    "c5_sedov3d_weno": Problem("c5_sedov3d_weno", 3, (16, 16, 16), (64, 64, 64), 3, RECON_WENO5, RIEMANN_HLLC,
+                               3, 0.3, bc=_OUT, ic="sedov", t_end=0.05),
+}
+
+
+# ----------------------------------------------------------------- layouts
+def to_global(p: Problem, A: np.ndarray) -> np.ndarray:
+    """Canonical [v][b][k][j][i] (b lexicographic over blocks) -> [v][Z][Y][X]."""
+    nv = A.shape[0]
+    nbx, nby, nbz = p.nblk
+    ni, nj, nk = p.nb
+    A = A.reshape(nv, nbz, nby, nbx, nk, nj, ni)
+    return A.transpose(0, 1, 4, 2, 5, 3, 6).reshape(nv, nbz * nk, nby * nj, nbx * ni)
+
+
+def from_global(p: Problem, G: np.ndarray) -> np.ndarray:
+    """[v][Z][Y][X] -> canonical [v][b][k][j][i]."""
+    nv = G.shape[0]
+    nbx, nby, nbz = p.nblk
+    ni, nj, nk = p.nb
+    G = G.reshape(nv, nbz, nk, nby, nj, nbx, ni)
+    return np.ascontiguousarray(G.transpose(0, 1, 3, 5, 2, 4, 6).reshape(nv, nbz * nby * nbx, nk, nj, ni))
+
+
+def centres(p: Problem):
+    """Cell-centre coordinates (x, y, z) as global [Z][Y][X] arrays."""
+    n = [p.nblk[d] * p.nb[d] for d in range(3)]
+    ax = []
+    for d in range(3):
+        h = (p.hi[d] - p.lo[d]) / n[d]
+        ax.append(p.lo[d] + (np.arange(n[d]) + 0.5) * h)
+    z, y, x = np.meshgrid(ax[2], ax[1], ax[0], indexing="ij")
+    return x, y, z
+
+
+def _prim_global(p: Problem, rho, vel, pres) -> np.ndarray:
+    shape = rho.shape
+    W = np.zeros((p.nvar,) + shape, dtype=np.float64)
+    W[0] = rho
+    for d in range(p.ndim):
+        W[1 + d] = vel[d] if vel is not None else 0.0
+    W[p.ndim + 1] = pres
+    return from_global(p, W)
+
+
+# -------------------------------------------------------------- generators
+def sod_x(p: Problem) -> np.ndarray:
+    """Sod along x (Toro 2009, Test 1): primitive W, canonical layout."""
+    x, _, _ = centres(p)
+    left = x < 0.5
+    rho = np.where(left, 1.0, 0.125)
+    pres = np.where(left, 1.0, 0.1)
+    return _prim_global(p, rho, None, pres)
+
+
+def sod_square(p: Problem) -> np.ndarray:
+    """Periodic square Sod: (1,0,1) inside |x-1/2|,|y-1/2| < 1/4, else (0.125,0,0.1)."""
+    x, y, _ = centres(p)
+    inside = (np.abs(x - 0.5) < 0.25) & (np.abs(y - 0.5) < 0.25)
+    rho = np.where(inside, 1.0, 0.125)
+    pres = np.where(inside, 1.0, 0.1)
+    return _prim_global(p, rho, None, pres)
+
+
+def sedov(p: Problem, e_blast: float = 1.0, p_amb: float = 1e-5, r0_cells: float = 3.5) -> np.ndarray:
+    """Sedov blast: E_blast deposited as uniform internal energy within r0 of the centre.
+
+    p_dep = (gamma-1) E_blast / (n_dep dV) is the IC's definition of the deposit
+    (an input recipe, not the method's EOS)."""
+    x, y, z = centres(p)
+    dxs = [(p.hi[d] - p.lo[d]) / (p.nblk[d] * p.nb[d]) for d in range(3)]
+    c = [0.5 * (p.lo[d] + p.hi[d]) for d in range(3)]
+    r2 = (x - c[0]) ** 2
+    if p.ndim >= 2:
+        r2 = r2 + (y - c[1]) ** 2
+    if p.ndim >= 3:
+        r2 = r2 + (z - c[2]) ** 2
+    r0 = r0_cells * dxs[0]
+    dep = r2 < r0 * r0
+    n_dep = int(dep.sum())
+    dV = float(np.prod(dxs[: p.ndim]))
+    rho = np.ones_like(x)
+    pres = np.full_like(x, p_amb)
+    pres[dep] = (p.gamma - 1.0) * e_blast / (n_dep * dV)
+    return _prim_global(p, rho, None, pres)
+
+
+def random_state(p: Problem, seed: int, blocky: bool = False) -> np.ndarray:
+    """rho, p ~ U[0.5,1.5]; u_d ~ U[-0.5,0.5]; 'blocky' adds x-jumps (rho x10, p x100)."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    n = [p.nblk[d] * p.nb[d] for d in range(3)]
+    shape = (n[2], n[1], n[0])
+    rho = g.uniform(0.5, 1.5, shape)
+    vel = [g.uniform(-0.5, 0.5, shape) for _ in range(p.ndim)]
+    pres = g.uniform(0.5, 1.5, shape)
+    if blocky:
+        edges, pos = [], 0
+        while pos < n[0]:
+            pos += int(g.integers(5, 14))
+            edges.append(pos)
+        seg = np.searchsorted(np.array(edges), np.arange(n[0]), side="right")
+        hi = (seg % 2 == 1)[None, None, :]
+        rho = np.where(hi, rho * 10.0, rho)
+        pres = np.where(hi, pres * 100.0, pres)
+    return _prim_global(p, rho, vel, pres)
+
+
+def uniform_state(p: Problem, seed: int) -> np.ndarray:
+    """A random constant (rho, u, p) everywhere."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    n = [p.nblk[d] * p.nb[d] for d in range(3)]
+    shape = (n[2], n[1], n[0])
+    rho = np.full(shape, g.uniform(0.5, 1.5))
+    vel = [np.full(shape, g.uniform(-0.5, 0.5)) for _ in range(p.ndim)]
+    pres = np.full(shape, g.uniform(0.5, 1.5))
+    return _prim_global(p, rho, vel, pres)
+
+
+def density_wave_avg(p: Problem, t: float = 0.0, amp: float = 0.2):
+    """Cell averages of rho = 1 + amp sin 2 pi (x - t), u = 1, p = 1 on [0,1] (1-D).
+
+    Returned as primitive W whose rho is the exact cell average (u, p are
+    constant, so the conserved cell averages follow linearly)."""
+    n = p.nblk[0] * p.nb[0]
+    h = (p.hi[0] - p.lo[0]) / n
+    xl = p.lo[0] + np.arange(n) * h
+    xr = xl + h
+    avg = 1.0 + amp * (np.cos(2 * math.pi * (xl - t)) - np.cos(2 * math.pi * (xr - t))) / (2 * math.pi * h)
+    rho = avg.reshape(1, 1, n)
+    vel = [np.ones_like(rho)]
+    pres = np.ones_like(rho)
+    return _prim_global(p, rho, vel, pres)
+
+
+def index_encoded(p: Problem) -> np.ndarray:
+    """U[v][g] = v * 2**32 + g (g = global cell index x + NX*(y + NY*z)); exact in fp64.
+
+    Used to prove guard-cell / block indexing bit-exact."""
+    n = [p.nblk[d] * p.nb[d] for d in range(3)]
+    g = np.arange(n[0] * n[1] * n[2], dtype=np.float64).reshape(n[2], n[1], n[0])
+    G = np.stack([v * 2.0 ** 32 + g for v in range(p.nvar)])
+    return from_global(p, G)
+
+
+def initial_primitive(p: Problem, seed: int = 0) -> np.ndarray:
+    if p.ic == "sod_x":
+        return sod_x(p)
+    if p.ic == "sod_square":
+        return sod_square(p)
+    if p.ic == "sedov":
+        return sedov(p)
+    if p.ic == "random":
+        return random_state(p, seed)
+    if p.ic == "blocky":
+        return random_state(p, seed, blocky=True)
+    raise ValueError(p.ic)
