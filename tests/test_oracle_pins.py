@@ -492,3 +492,44 @@ def test_nonphysical_detected():
     U[0, 0, 0, 0, 3] = -1.0  # negative density
     with pytest.raises(oracle.OracleError):
         oracle.step(p.config(), U, dt_fixed=1e-3)
+
+
+def test_rotation_invariance_3d():
+    """A 1-D profile with constant transverse velocities, laid along x, y or z of
+    a 3-D periodic box, evolves identically (to round-off) in each orientation:
+    pins the rotated frame of every direction (normal / transverse components and
+    the full |u|^2 in the energy)."""
+    N = 32
+    g = np.random.Generator(np.random.PCG64(21))
+    rho = g.uniform(0.5, 1.5, N) * np.where(np.arange(N) % 11 < 5, 1.0, 4.0)
+    pres = g.uniform(0.5, 1.5, N) * np.where(np.arange(N) % 7 < 3, 1.0, 10.0)
+    un = g.uniform(-0.5, 0.5, N)
+    ut1, ut2 = 0.3, -0.45
+    res = []
+    for axis in range(3):
+        nb = [4, 4, 4]
+        nblk = [1, 1, 1]
+        nb[axis], nblk[axis] = 8, N // 8
+        p = si.Problem("rot", 3, tuple(nb), tuple(nblk), 3, 2, 1, 3, 0.3, bc=((0, 0),) * 3)
+        shape = [4, 4, 4]
+        shape[axis] = N
+        sh = (shape[2], shape[1], shape[0])
+        bshape = [1, 1, 1]
+        bshape[2 - axis] = N
+        line = lambda a: np.broadcast_to(np.asarray(a, dtype=float).reshape(bshape) if np.ndim(a) else a, sh)
+        vel = [None, None, None]
+        tr = iter([ut1, ut2])
+        for d in range(3):
+            vel[d] = line(un) if d == axis else line(next(tr))
+        W = np.stack([line(rho), vel[0], vel[1], vel[2], line(pres)]).astype(float)
+        U0 = cons(p, si.from_global(p, W))
+        U, _ = oracle.step(p.config(), U0, dt_fixed=2e-3)
+        U, _ = oracle.step(p.config(), U, dt_fixed=2e-3)
+        G = si.to_global(p, U)
+        idx = [0, 0, 0]
+        idx[2 - axis] = slice(None)
+        prof = G[(slice(None),) + tuple(idx)]          # [v][N]
+        order = [0, 1 + axis] + [1 + d for d in range(3) if d != axis] + [4]
+        res.append(prof[order])
+    for r in res[1:]:
+        assert np.allclose(r, res[0], rtol=1e-13, atol=1e-14)
