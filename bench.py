@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark of the Spark block-update hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl reference]
+
+One "step" = one full SSP-RK step (every stage: guard-cell exchange + fused
+stage kernel over all blocks; the dt of the next step fused into the last
+stage) of the whole synthetic workload.  N = 1: configs[3] (3-D Sedov 256^3 in
+16^3 blocks, PLM + HLLC + SSP-RK2 by default; --config c4_sedov3d_weno for
+WENO5/RK3).  N > 1 (torchrun, one rank per GPU): weak scaling, 256^3 per GPU,
+the global block grid grown along the process grid, NCCL halo exchange + dt
+all-reduce.  Prints ONE JSON line on rank 0.
+
+metric  zone-updates/s = interior cells x RK stages x steps / time (all ranks)
+value   device time (CUDA events on the library stream, barrier + sync on both
+        sides, max over ranks), inputs resident in HBM; the 640 MiB state per
+        copy is > L2 (126 MB), so no L2 flush is needed between steps.
+e2e     same metric through the public API with HOST buffers: every step
+        uploads the state from pinned host memory (spark_set_state), steps,
+        and reads it back (spark_get_state).
+--impl reference   the CPU oracle (oracle/, the reference arm of this tier) on
+        a bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import spark_inputs as si  # noqa: E402
+
+METRIC = "zone-updates/sec (cells×RK stages) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "zone-updates/s"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def algorithmic_bytes_per_zone(p: si.Problem, stage: int) -> int:
+    """HBM bytes the method itself must move per zone-update:
+    stage 1 reads U^n and writes U^(1); later stages read U^(s-1) and U^n and
+    write U^(s).  Halo re-reads are L2 traffic, dt is fused."""
+    return (2 if stage == 1 else 3) * p.nvar * 8
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def ncu_traffic(name: str):
+    """dram bytes per stage-kernel launch from the committed ncu summary (or None)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.out = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self):
+        if not self.out:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def problem_for(args, world: int) -> si.Problem:
+    p = si.PRESETS[args.config]
+    if world > 1:
+        # weak scaling: 256^3 (16^3 blocks of 16^3) per GPU along a process grid
+        pg = {2: (1, 1, 2), 4: (1, 2, 2), 8: (2, 2, 2)}.get(world)
+        if pg is None:
+            pg = (1, 1, world)
+        p = p.with_(nblk=tuple(p.nblk[d] * pg[d] for d in range(3)),
+                    hi=tuple(p.hi[d] * pg[d] for d in range(3)))
+    return p
+
+
+# ---------------------------------------------------------------- oracle leg
+def oracle_sample(p: si.Problem, budget_s: float, max_steps: int = 1000):
+    """Time the oracle (as it stands) on a bounded sample of the workload:
+    the same scheme / block shape on a 4x4x4-block (64^3) sub-grid of Sedov."""
+    import oracle
+
+    q = p.with_(nblk=tuple(min(4, p.nblk[d]) for d in range(3)))
+    U = oracle.prim_to_cons(q.ndim, q.gamma, si.initial_primitive(q))
+    U, _ = oracle.step(q.config(), U)  # warm-up (page-in, thread pool)
+    t0 = time.perf_counter()
+    steps = 0
+    while steps < max_steps:
+        U, _ = oracle.step(q.config(), U)
+        steps += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    el = time.perf_counter() - t0
+    zu = q.ncells * q.rk_stages * steps
+    return zu / el, oracle.num_threads(), f"{q.nb[0]}^3 blocks x {q.nblk[0]}x{q.nblk[1]}x{q.nblk[2]} " \
+        f"({q.ncells} cells, {q.name} scheme, Sedov), {steps} steps, {el:.1f} s"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    p = problem_for(args, 1)
+    import oracle
+
+    oracle.build()
+    q = p.with_(nblk=tuple(min(4, p.nblk[d]) for d in range(3)))
+    U = oracle.prim_to_cons(q.ndim, q.gamma, si.initial_primitive(q))
+    for _ in range(args.warmup):
+        U, _ = oracle.step(q.config(), U)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        U, _ = oracle.step(q.config(), U)
+    el = time.perf_counter() - t0
+    zu = q.ncells * q.rk_stages * args.steps
+    v = zu / el
+    sample = f"{q.ncells}-cell sub-grid ({q.nblk[0]}x{q.nblk[1]}x{q.nblk[2]} blocks of 16^3) of {p.name}"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": p.name, "cells": p.ncells, "sampled_cells": q.ncells, "rk_stages": p.rk_stages},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------- GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4_sedov3d_plm", choices=sorted(si.PRESETS))
+    ap.add_argument("--impl", default="spark", choices=["spark", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_03378_b200 import spark
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    p = problem_for(args, world)
+    cfg = p.config()
+    nccl_id = None
+    if world > 1:
+        obj = [spark.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    stream = torch.cuda.Stream()
+    lo, n = spark.rank_box(cfg, rank, world)
+    box = (tuple(lo[d] * p.nb[d] for d in range(3)), tuple(n[d] * p.nb[d] for d in range(3)))
+    W = si.initial_primitive(p, box=box if world > 1 else None)
+    with torch.cuda.stream(stream):
+        s = spark.Spark(cfg, rank, world, nccl_id=nccl_id, device=local, stream=stream)
+        Wd = torch.from_numpy(W).to(f"cuda:{local}")
+        s.set_primitive(Wd)
+        stream.synchronize()
+        del Wd
+    cells_local = int(np.prod(W.shape[1:]))
+    zu_per_step = p.ncells * p.rk_stages  # all ranks
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        s.step()
+    stream.synchronize()
+
+    # ---- timed region (device time on the library stream)
+    s.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            s.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    stage_ms, stage_launches, total_launches = s.profile_read()
+    s.profile(False)
+    t_dev = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+    ms = float(t_dev.item())
+    value = zu_per_step * args.steps / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (the fused stage kernel)
+    peaks, peak_kind = measured_peaks()
+    bytes_per_step_local = sum(algorithmic_bytes_per_zone(p, st) for st in range(1, p.rk_stages + 1)) * cells_local
+    bytes_per_launch = bytes_per_step_local / p.rk_stages
+    avg_launch_s = stage_ms * 1e-3 / max(stage_launches, 1)
+    achieved = bytes_per_launch / avg_launch_s / 1e9
+    traffic = ncu_traffic(p.name)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "kernel": "stage_kernel (KB1)", "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
+                "stage_kernel_share": (stage_ms / ms) if ms > 0 else None}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if world >= 1:
+        hostU = torch.empty(s.shape, dtype=torch.float64).pin_memory()
+        s.get_state(out=hostU.numpy())
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            s.set_state(hostU.numpy())
+            s.step()
+            s.get_state(out=hostU.numpy())
+        torch.cuda.synchronize()
+        barrier()
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        el = float(el.item())
+        nbytes = int(np.prod(s.shape)) * 8
+        e2e = {"value": zu_per_step * args.e2e_steps / el, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
+               "note": "per step: spark_set_state from pinned host + spark_step + spark_get_state to pinned host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample = oracle_sample(p, args.cpu_budget)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": p.name, "cells": p.ncells, "cells_per_gpu": cells_local,
+                       "block": list(p.nb), "blocks": list(p.nblk), "recon": ["first", "plm", "weno5"][p.recon],
+                       "riemann": ["hll", "hllc"][p.riemann], "rk_stages": p.rk_stages, "ng": p.ng,
+                       "parallelism": f"blocks over {world} GPU(s)", "l2": "state per copy > L2 (no flush needed)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": total_launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

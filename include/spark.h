@@ -1,0 +1,227 @@
+/*
+ * spark.h — C ABI of libspark, the B200-native Spark block-update hot path.
+ *
+ * What the library computes (PAPER.md = arXiv 2401.03378, /root/reference):
+ *   Flash-X's Spark hydrodynamics solver advances a set of blocks of identical
+ *   cell counts, each surrounded by a halo of guard cells that makes it look
+ *   like a whole domain (§2.2), with strong-stability-preserving
+ *   Runge-Kutta stages (§4.2).  In the non-telescoping variant
+ *   (lst:spark-nontelescoping) every stage first fills the guard
+ *   cells ("p2p communication") and then runs, for all blocks, the
+ *   block initialisation (Alg. 7) and the intra-stage chain of
+ *   Alg. 8: calcLims (reconstruction) -> calcFlux (Riemann) ->
+ *   updSoln (divergence + RK combination) -> calcEos.  The paper prints no
+ *   formulas; the numerics are the textbook readings in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *   - Every function returns spark_status; no C++ exception crosses the ABI.
+ *     After an error, spark_last_error(ctx) describes it (ctx-owned string).
+ *   - Layouts, fp64 throughout:
+ *       canonical  U[v][b][k][j][i]   i fastest; b = bx + nbx*(by + nby*bz)
+ *                  lexicographic over THIS RANK's sub-box of the block grid.
+ *       padded     P[v][b][k+gz][j+gy][i+gx], gd = ng for d < ndim else 0
+ *                  (the Flash-X block-with-guards of P:361-364).
+ *     v = 0 density, 1..ndim momentum, ndim+1 total energy (conserved) or
+ *     v = 0 density, 1..ndim velocity, ndim+1 pressure (primitive).
+ *   - Memory ownership: the CALLER owns the device arena passed to spark_init
+ *     (>= spark_required_bytes) and keeps it alive until spark_finalize.  The
+ *     library never allocates device memory for state and never frees caller
+ *     memory.  Host/device pointers passed to other calls are borrowed for the
+ *     duration of the call.
+ *   - Streams: all device work is enqueued on the cudaStream_t given to
+ *     spark_init.  Only calls documented as synchronising block the host.
+ *   - Determinism: identical inputs and rank count give bitwise-identical
+ *     results; no floating-point atomics are used (dt minimum via integer
+ *     atomics on the ordered bit pattern of positive doubles).  Results are
+ *     also bitwise independent of the rank count (halos are exact copies).
+ *   - Thread safety: one context per device per host thread; not re-entrant.
+ */
+#ifndef SPARK_H
+#define SPARK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPARK_ABI_VERSION 1
+
+typedef enum {
+    SPARK_OK = 0,
+    SPARK_ERR_ARG = 1,          /* invalid argument or configuration            */
+    SPARK_ERR_CUDA = 2,         /* CUDA runtime error (message in last_error)   */
+    SPARK_ERR_NCCL = 3,         /* NCCL error                                   */
+    SPARK_ERR_OOM = 4,          /* arena too small                              */
+    SPARK_ERR_NONPHYSICAL = 5,  /* rho <= 0, p <= 0 or non-finite after a stage */
+    SPARK_ERR_STATE = 6         /* call out of order (e.g. step before state)   */
+} spark_status;
+
+typedef enum { SPARK_BC_PERIODIC = 0, SPARK_BC_OUTFLOW = 1, SPARK_BC_REFLECT = 2 } spark_bc;
+typedef enum { SPARK_RECON_FIRST = 0, SPARK_RECON_PLM = 1, SPARK_RECON_WENO5 = 2 } spark_recon;
+typedef enum { SPARK_RIEMANN_HLL = 0, SPARK_RIEMANN_HLLC = 1 } spark_riemann;
+
+/* Problem description.  Identical on every rank (it describes the GLOBAL grid). */
+typedef struct {
+    int32_t ndim;         /* 1..3; nvar = ndim + 2                                   */
+    int32_t nb[3];        /* interior cells per block per dim (1 for d >= ndim)      */
+    int32_t nblk[3];      /* blocks per dim of the global grid (1 for d >= ndim)     */
+    int32_t ng;           /* guard layers: >= 1 first order, >= 2 PLM, >= 3 WENO5    */
+    double lo[3], hi[3];  /* domain; dx_d = (hi_d - lo_d) / (nblk_d * nb_d)          */
+    int32_t bc[3][2];     /* spark_bc per face (low, high) per dim                   */
+    int32_t recon;        /* spark_recon                                             */
+    int32_t riemann;      /* spark_riemann                                           */
+    int32_t rk_stages;    /* 2 (SSP-RK2) or 3 (SSP-RK3)                              */
+    double gamma;         /* ideal-gas ratio of specific heats (> 1)                 */
+    double cfl;           /* Courant number C in dt = C min dx_d/(|u_d| + c)         */
+} spark_config;
+
+typedef struct spark_ctx spark_ctx; /* opaque, one per rank (per GPU) */
+
+/* Halo plan of one face of a rank's sub-box (host-side, no GPU needed). */
+typedef struct {
+    int32_t dim, side;    /* face: dimension 0..2, side 0 = low, 1 = high           */
+    int32_t peer;         /* rank across the face; -1 = physical boundary / self    */
+    int32_t pad;
+    int64_t cells;        /* cells in the ng-thick slab (0 when peer < 0)           */
+} spark_face_plan;
+
+/* ---- host-only queries (valid on machines without a GPU) -------------- */
+
+int32_t spark_abi_version(void);
+const char* spark_status_string(spark_status st);
+
+/* Validate a configuration for nranks ranks.  Checks ndim, nb >= ng, ng large
+ * enough for recon, rk_stages, gamma > 1, cfl > 0, the block grid divisible
+ * by the process grid, and nb[0]*nb[1] <= 1024 (one CTA thread per column). */
+spark_status spark_check_config(const spark_config* cfg, int32_t nranks);
+
+/* Process grid (P_x, P_y, P_z) used for nranks ranks: the factorisation of
+ * nranks that divides the block grid and minimises the halo surface. */
+spark_status spark_rank_grid(const spark_config* cfg, int32_t nranks, int32_t pgrid[3]);
+
+/* Sub-box of `rank` in BLOCK units: first block box_lo[d], count box_n[d].
+ * Ranks are ordered x fastest over the process grid. */
+spark_status spark_rank_box(const spark_config* cfg, int32_t rank, int32_t nranks,
+                            int32_t box_lo[3], int32_t box_n[3]);
+
+/* The 2*ndim face plans of `rank` (faces ordered dim-major, low then high).
+ * A slab holds ng layers of the face cells, layout [v][c2][c1][c0] with c_dim
+ * of extent ng (depth in increasing global coordinate) and the other two of
+ * the sub-box extent in cells. */
+spark_status spark_halo_plan(const spark_config* cfg, int32_t rank, int32_t nranks,
+                             spark_face_plan faces[6], int32_t* nfaces);
+
+/* Device bytes the caller must provide as the arena of spark_init. */
+spark_status spark_required_bytes(const spark_config* cfg, int32_t rank, int32_t nranks,
+                                  size_t* bytes);
+
+/* ---- lifecycle ---------------------------------------------------------- */
+
+/* Rank 0 creates the NCCL unique id (128 bytes); the harness broadcasts it. */
+spark_status spark_nccl_unique_id(uint8_t id[128]);
+
+/* Create a context on CUDA device `device`.  nranks == 1: nccl_id may be NULL.
+ * nranks > 1: nccl_id from spark_nccl_unique_id on rank 0 (collective call:
+ * every rank must call spark_init).  cuda_stream is a cudaStream_t (NULL =
+ * legacy default stream).  arena: device memory of >= required bytes, owned
+ * by the caller.  Does not synchronise except for NCCL communicator setup. */
+spark_status spark_init(const spark_config* cfg, int32_t rank, int32_t nranks, const uint8_t* nccl_id,
+                        int32_t device, void* cuda_stream, void* arena, size_t arena_bytes,
+                        spark_ctx** out);
+
+/* Virtual ranks on ONE device in one process (testing the multi-rank path
+ * without several GPUs): creates nranks contexts whose halo exchange is a
+ * device-to-device copy between their buffers.  arenas[r] as in spark_init.
+ * Contexts made this way must be stepped with spark_step_group. */
+spark_status spark_init_local_group(const spark_config* cfg, int32_t nranks, int32_t device,
+                                    void* cuda_stream, void* const* arenas, size_t arena_bytes,
+                                    spark_ctx** outs);
+
+/* Release the context (NCCL communicator, events).  Does not free the arena.
+ * Synchronises the stream. */
+spark_status spark_finalize(spark_ctx* ctx);
+
+/* Last error message of this context ("" if none).  Owned by ctx. */
+const char* spark_last_error(const spark_ctx* ctx);
+
+/* ---- state I/O ------------------------------------------------------------ */
+
+/* Load this rank's conserved state U (canonical layout, nvar*ncells_local
+ * doubles).  on_device != 0: U is a device pointer, else host memory (pinned
+ * for asynchronous copies).  Resets t = 0 and the step count, clears the
+ * status word, and computes the CFL minimum of U (KB3) followed by the
+ * global-min all-reduce.  Enqueued asynchronously; host U must stay valid
+ * until the stream reaches the copy. */
+spark_status spark_set_state(spark_ctx* ctx, const double* U, int32_t on_device);
+
+/* As spark_set_state, but from primitive variables W (rho, u, p) converted on
+ * the device with the ideal-gas EOS: E = p/(gamma-1) + rho|u|^2/2. */
+spark_status spark_set_primitive(spark_ctx* ctx, const double* W, int32_t on_device);
+
+/* Copy the current conserved state U^n into U (canonical layout).
+ * SYNCHRONISES the stream; returns SPARK_ERR_NONPHYSICAL if the status word
+ * reports a non-physical state. */
+spark_status spark_get_state(spark_ctx* ctx, double* U, int32_t on_device);
+
+/* Time, completed steps and dt of the last step.  Synchronises. */
+spark_status spark_get_time(spark_ctx* ctx, double* t, int64_t* steps, double* dt_last);
+
+/* Raw CFL minimum min_cells min_d dx_d/(|u_d|+c) of U^n over all ranks (what
+ * dt = cfl * value is built from).  Synchronises. */
+spark_status spark_get_cfl_min(spark_ctx* ctx, double* value);
+
+/* ---- the hot path -------------------------------------------------------- */
+
+/* fill_guardcells: exchange the rank-boundary face
+ * slabs of U^n with the neighbouring ranks.  padded_out != NULL (device
+ * pointer, padded layout): additionally materialise every block with its
+ * guard cells (faces, edges, corners; each guard cell = the per-dimension
+ * boundary map of its global index, reflect negating the normal momentum).
+ * With nranks > 1 edge/corner guards owned by diagonal ranks are left NaN.
+ * Bit-exact copies.  Asynchronous. */
+spark_status spark_fill_guardcells(spark_ctx* ctx, double* padded_out);
+
+/* One SSP-RK step (lst:spark-nontelescoping): for each stage, guard-cell
+ * exchange then the fused stage kernel over all blocks.  dt > 0: use it;
+ * dt <= 0: CFL dt of U^n (cfl * global min), clipped to t_end - t when
+ * t_end > 0; once t >= t_end*(1 - 1e-14) further steps leave U unchanged.
+ * dt_used == NULL: fully asynchronous.  dt_used != NULL: synchronises, writes
+ * the dt taken and checks the status word; on SPARK_ERR_NONPHYSICAL the state
+ * is rolled back to U^n of this step. */
+spark_status spark_step(spark_ctx* ctx, double dt, double t_end, double* dt_used);
+
+/* Enqueue up to max_steps steps (CFL dt, clipped to t_end), synchronising
+ * every check_every steps (<= 0: only at the end) to stop once t_end is
+ * reached.  *steps_done receives the number of steps that advanced time. */
+spark_status spark_advance(spark_ctx* ctx, int64_t max_steps, double t_end, int32_t check_every,
+                           int64_t* steps_done);
+
+/* spark_step for the contexts of one spark_init_local_group, stage by stage
+ * in lockstep (exchange between virtual ranks, global dt minimum). */
+spark_status spark_step_group(spark_ctx* const* ctxs, int32_t n, double dt, double t_end, double* dt_used);
+
+/* Apply ONE fused stage to caller buffers (device pointers, canonical layout):
+ *   U_out = a * U_n + b * (U_prev + dt * L(U_prev))
+ * with guard cells of U_prev from the boundary maps (single-rank contexts
+ * only).  U_n may be NULL when a == 0.  For testing the stage in isolation.
+ * Asynchronous. */
+spark_status spark_stage_apply(spark_ctx* ctx, const double* U_prev, const double* U_n, double a, double b,
+                               double dt, double* U_out);
+
+/* ---- measurement ----------------------------------------------------------- */
+
+/* Enable/disable CUDA-event timing around every launch of the fused stage
+ * kernel (on the context stream); resets the accumulators when enabling. */
+spark_status spark_profile_enable(spark_ctx* ctx, int32_t on);
+
+/* Accumulated stage-kernel time (ms) and launches since enabling.
+ * Synchronises. */
+spark_status spark_profile_read(spark_ctx* ctx, double* stage_ms, int64_t* stage_launches,
+                                int64_t* total_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARK_H */

@@ -1,0 +1,820 @@
+// spark_api.cpp — host layer and C ABI of libspark (include/spark.h).
+//
+// Owns: configuration checks, the rank decomposition (process grid over the
+// global block grid, "blocks distributed variably among
+// computational resources"), the arena sub-allocation, the SSP-RK stage loop of
+// lst:spark-nontelescoping (guard-cell fill before every stage,
+// then all blocks), buffer rotation, the halo exchange (NCCL grouped
+// send/recv over NVLink, or device copies between virtual ranks) and the dt
+// all-reduce (ncclMin on the ordered bits of the CFL minimum).
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/spark.h"
+#include "spark_internal.h"
+
+namespace {
+
+struct Error : std::runtime_error {
+    spark_status st;
+    Error(spark_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+#define CU(call)                                                                                        \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess)                                                                          \
+            throw Error(SPARK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+
+#define NC(call)                                                                                        \
+    do {                                                                                                \
+        ncclResult_t r_ = (call);                                                                       \
+        if (r_ != ncclSuccess)                                                                          \
+            throw Error(SPARK_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));            \
+    } while (0)
+
+int stencil_ng(int recon) { return recon == SPARK_RECON_WENO5 ? 3 : (recon == SPARK_RECON_PLM ? 2 : 1); }
+
+std::string check(const spark_config* c, int nranks) {
+    if (!c) return "null config";
+    if (c->ndim < 1 || c->ndim > 3) return "ndim must be 1..3";
+    if (nranks < 1) return "nranks must be >= 1";
+    if (c->recon < 0 || c->recon > 2) return "unknown recon";
+    if (c->riemann < 0 || c->riemann > 1) return "unknown riemann";
+    if (c->rk_stages != 2 && c->rk_stages != 3) return "rk_stages must be 2 or 3";
+    if (!(c->gamma > 1.0)) return "gamma must be > 1";
+    if (!(c->cfl > 0.0)) return "cfl must be > 0";
+    if (c->ng < stencil_ng(c->recon)) return "ng too small for the reconstruction";
+    for (int d = 0; d < 3; d++) {
+        if (c->nb[d] < 1 || c->nblk[d] < 1) return "nb and nblk must be >= 1";
+        if (d >= c->ndim && (c->nb[d] != 1 || c->nblk[d] != 1)) return "unused dims need nb = nblk = 1";
+        if (d < c->ndim && c->nb[d] < c->ng) return "nb must be >= ng";
+        if (d < c->ndim && !(c->hi[d] > c->lo[d])) return "hi must exceed lo";
+        for (int s = 0; s < 2; s++)
+            if (c->bc[d][s] < 0 || c->bc[d][s] > 2) return "unknown boundary condition";
+        if (d < c->ndim && (c->bc[d][0] == SPARK_BC_PERIODIC) != (c->bc[d][1] == SPARK_BC_PERIODIC))
+            return "periodic boundaries must be periodic on both sides";
+    }
+    const long long plane = (long long)c->nb[0] * (c->ndim >= 2 ? c->nb[1] : 1);
+    if (plane > 256) return "nb[0]*nb[1] must be <= 256 (one thread per column)";
+    const long long cells = (long long)c->nb[0] * c->nb[1] * c->nb[2] * c->nblk[0] * c->nblk[1] * c->nblk[2];
+    if (cells > (1LL << 40)) return "grid too large";
+    for (int d = 0; d < 3; d++)
+        if ((long long)c->nb[d] * c->nblk[d] > INT_MAX / 2) return "grid too large";
+    return "";
+}
+
+// Process grid: factorisation of nranks dividing the block grid, minimising
+// the exchanged surface; ties prefer splitting the slowest-varying dim.
+bool rank_grid(const spark_config* c, int nranks, int pg[3]) {
+    long long best = -1;
+    bool found = false;
+    for (int pz = 1; pz <= nranks; pz++) {
+        if (nranks % pz) continue;
+        for (int py = 1; py <= nranks / pz; py++) {
+            if ((nranks / pz) % py) continue;
+            const int px = nranks / pz / py;
+            const int p[3] = {px, py, pz};
+            bool ok = true;
+            for (int d = 0; d < 3; d++)
+                if (c->nblk[d] % p[d] || (d >= c->ndim && p[d] != 1)) ok = false;
+            if (!ok) continue;
+            long long n[3];
+            for (int d = 0; d < 3; d++) n[d] = (long long)c->nb[d] * c->nblk[d] / p[d];
+            long long surf = 0;
+            for (int d = 0; d < c->ndim; d++)
+                if (p[d] > 1 || c->bc[d][0] == SPARK_BC_PERIODIC) {
+                    long long f = 1;
+                    for (int e = 0; e < c->ndim; e++)
+                        if (e != d) f *= n[e];
+                    if (p[d] > 1) surf += 2 * f;
+                }
+            if (!found || surf < best || (surf == best && pz > pg[2]) ||
+                (surf == best && pz == pg[2] && py > pg[1])) {
+                best = surf;
+                pg[0] = px;
+                pg[1] = py;
+                pg[2] = pz;
+                found = true;
+            }
+        }
+    }
+    return found;
+}
+
+struct Plan {
+    int pg[3], pc[3], box_lo[3], box_n[3];
+    int peer[3][2];  // -1: no peer (physical boundary or periodic self-wrap)
+    spark::Geo geo;
+};
+
+Plan make_plan(const spark_config* c, int rank, int nranks) {
+    std::string m = check(c, nranks);
+    if (!m.empty()) throw Error(SPARK_ERR_ARG, m);
+    if (rank < 0 || rank >= nranks) throw Error(SPARK_ERR_ARG, "rank out of range");
+    Plan p{};
+    if (!rank_grid(c, nranks, p.pg)) throw Error(SPARK_ERR_ARG, "block grid not divisible among ranks");
+    p.pc[0] = rank % p.pg[0];
+    p.pc[1] = (rank / p.pg[0]) % p.pg[1];
+    p.pc[2] = rank / (p.pg[0] * p.pg[1]);
+    spark::Geo& g = p.geo;
+    g.ndim = c->ndim;
+    g.nvar = c->ndim + 2;
+    g.ng = c->ng;
+    g.cpb = 1;
+    g.ncell = 1;
+    for (int d = 0; d < 3; d++) {
+        p.box_n[d] = c->nblk[d] / p.pg[d];
+        p.box_lo[d] = p.pc[d] * p.box_n[d];
+        g.nb[d] = c->nb[d];
+        g.bn[d] = p.box_n[d];
+        g.cn[d] = c->nb[d] * p.box_n[d];
+        g.gN[d] = c->nb[d] * c->nblk[d];
+        g.off[d] = p.box_lo[d] * c->nb[d];
+        g.cpb *= c->nb[d];
+        g.ncell *= g.cn[d];
+        g.dx[d] = (c->hi[d] - c->lo[d]) / ((double)c->nblk[d] * (double)c->nb[d]);
+        g.rdx[d] = 1.0 / g.dx[d];
+        for (int s = 0; s < 2; s++) {
+            g.bc[d][s] = c->bc[d][s];
+            p.peer[d][s] = -1;
+            g.halo[d][s] = 0;
+        }
+    }
+    for (int d = 0; d < c->ndim; d++) {
+        for (int s = 0; s < 2; s++) {
+            int q[3] = {p.pc[0], p.pc[1], p.pc[2]};
+            q[d] += s ? 1 : -1;
+            if (q[d] < 0 || q[d] >= p.pg[d]) {
+                if (c->bc[d][s] != SPARK_BC_PERIODIC || p.pg[d] == 1) continue;  // local boundary map
+                q[d] = (q[d] + p.pg[d]) % p.pg[d];
+            }
+            p.peer[d][s] = q[0] + p.pg[0] * (q[1] + p.pg[1] * q[2]);
+            g.halo[d][s] = 1;
+        }
+    }
+    for (int d = 0; d < 3; d++) {
+        long long s = g.ng;
+        for (int e = 0; e < 3; e++)
+            if (e != d) s *= g.cn[e];
+        g.slab[d] = d < c->ndim ? s : 0;
+    }
+    g.gamma = c->gamma;
+    g.cfl = c->cfl;
+    return p;
+}
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+size_t arena_bytes(const Plan& p) {
+    const size_t state = align_up(sizeof(double) * p.geo.nvar * (size_t)p.geo.ncell);
+    size_t halo = 0;
+    for (int d = 0; d < 3; d++)
+        for (int s = 0; s < 2; s++)
+            if (p.peer[d][s] >= 0) halo += 2 * align_up(sizeof(double) * p.geo.nvar * (size_t)p.geo.slab[d]);
+    return align_up(sizeof(spark::DevScalars)) + 3 * state + halo;
+}
+
+struct LocalGroup {
+    std::vector<spark_ctx*> members;
+};
+
+}  // namespace
+
+struct spark_ctx {
+    spark_config cfg{};
+    int rank = 0, nranks = 1, device = 0;
+    cudaStream_t stream = nullptr;
+    Plan plan{};
+    double* U[3] = {nullptr, nullptr, nullptr};
+    int n_idx = 0;
+    double* send[3][2] = {};
+    double* recv[3][2] = {};
+    spark::DevScalars* sc = nullptr;
+    ncclComm_t comm = nullptr;
+    std::shared_ptr<LocalGroup> group;
+    bool have_state = false;
+    std::string err;
+    // profiling
+    bool prof = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    size_t ev_used = 0;
+    int64_t stage_launches = 0, total_launches = 0;
+    double prof_ms = 0.0;
+};
+
+namespace {
+
+spark_status fail(spark_ctx* ctx, const Error& e) {
+    if (ctx) ctx->err = e.what();
+    return e.st;
+}
+
+template <typename F>
+spark_status guard(spark_ctx* ctx, F&& f) {
+    try {
+        if (ctx) ctx->err.clear();
+        f();
+        return SPARK_OK;
+    } catch (const Error& e) {
+        return fail(ctx, e);
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return SPARK_ERR_ARG;
+    } catch (...) {
+        if (ctx) ctx->err = "unknown error";
+        return SPARK_ERR_ARG;
+    }
+}
+
+void set_device(spark_ctx* c) { CU(cudaSetDevice(c->device)); }
+
+void launched(spark_ctx* c, cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error(SPARK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    c->total_launches++;
+}
+
+void carve(spark_ctx* c, void* arena, size_t bytes) {
+    const size_t need = arena_bytes(c->plan);
+    if (!arena) throw Error(SPARK_ERR_ARG, "null arena");
+    if (bytes < need) throw Error(SPARK_ERR_OOM, "arena smaller than spark_required_bytes");
+    if (reinterpret_cast<uintptr_t>(arena) % 16) throw Error(SPARK_ERR_ARG, "arena must be 16-byte aligned");
+    char* p = static_cast<char*>(arena);
+    const spark::Geo& g = c->plan.geo;
+    c->sc = reinterpret_cast<spark::DevScalars*>(p);
+    p += align_up(sizeof(spark::DevScalars));
+    const size_t state = align_up(sizeof(double) * g.nvar * (size_t)g.ncell);
+    for (int i = 0; i < 3; i++) {
+        c->U[i] = reinterpret_cast<double*>(p);
+        p += state;
+    }
+    for (int d = 0; d < 3; d++)
+        for (int s = 0; s < 2; s++)
+            if (c->plan.peer[d][s] >= 0) {
+                const size_t sb = align_up(sizeof(double) * g.nvar * (size_t)g.slab[d]);
+                c->send[d][s] = reinterpret_cast<double*>(p);
+                p += sb;
+                c->recv[d][s] = reinterpret_cast<double*>(p);
+                p += sb;
+            }
+}
+
+spark_ctx* make_ctx(const spark_config* cfg, int rank, int nranks, int device, void* stream, void* arena,
+                    size_t bytes) {
+    auto c = std::make_unique<spark_ctx>();
+    c->cfg = *cfg;
+    c->rank = rank;
+    c->nranks = nranks;
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(stream);
+    c->plan = make_plan(cfg, rank, nranks);
+    carve(c.get(), arena, bytes);
+    set_device(c.get());
+    launched(c.get(), spark::launch_scalars_reset(c->sc, c->stream), "scalars reset");
+    return c.release();
+}
+
+// -------------------------------------------------------------- exchange
+void pack_all(spark_ctx* c, const double* u) {
+    for (int d = 0; d < 3; d++)
+        for (int s = 0; s < 2; s++)
+            if (c->plan.peer[d][s] >= 0)
+                launched(c, spark::launch_pack(c->plan.geo, u, d, s, c->send[d][s], c->stream), "pack");
+}
+
+// NCCL grouped send/recv.  Per dim: [send high slab -> high peer, recv low
+// halo <- low peer, send low slab -> low peer, recv high halo <- high peer];
+// posting in the same order on every rank matches messages between the same
+// pair of ranks (P_d = 2 periodic: both faces have the same peer).
+void exchange_nccl(spark_ctx* c) {
+    const spark::Geo& g = c->plan.geo;
+    NC(ncclGroupStart());
+    for (int d = 0; d < 3; d++) {
+        const size_t n = (size_t)g.nvar * g.slab[d];
+        if (c->plan.peer[d][1] >= 0) NC(ncclSend(c->send[d][1], n, ncclFloat64, c->plan.peer[d][1], c->comm, c->stream));
+        if (c->plan.peer[d][0] >= 0) NC(ncclRecv(c->recv[d][0], n, ncclFloat64, c->plan.peer[d][0], c->comm, c->stream));
+        if (c->plan.peer[d][0] >= 0) NC(ncclSend(c->send[d][0], n, ncclFloat64, c->plan.peer[d][0], c->comm, c->stream));
+        if (c->plan.peer[d][1] >= 0) NC(ncclRecv(c->recv[d][1], n, ncclFloat64, c->plan.peer[d][1], c->comm, c->stream));
+    }
+    NC(ncclGroupEnd());
+}
+
+// Virtual ranks: recv(d, s) of rank r <- send(d, 1-s) of its peer.
+void exchange_local(const std::vector<spark_ctx*>& m) {
+    for (spark_ctx* c : m) {
+        const spark::Geo& g = c->plan.geo;
+        for (int d = 0; d < 3; d++)
+            for (int s = 0; s < 2; s++) {
+                const int peer = c->plan.peer[d][s];
+                if (peer < 0) continue;
+                const size_t bytes = sizeof(double) * g.nvar * (size_t)g.slab[d];
+                CU(cudaMemcpyAsync(c->recv[d][s], m[peer]->send[d][1 - s], bytes, cudaMemcpyDeviceToDevice,
+                                   c->stream));
+            }
+    }
+}
+
+void allreduce_acc(spark_ctx* c) {
+    if (c->nranks > 1 && c->comm)
+        NC(ncclAllReduce(&c->sc->acc, &c->sc->acc, 1, ncclUint64, ncclMin, c->comm, c->stream));
+}
+
+// Local group: every member's acc <- min over members (tiny host-side launch
+// of a device copy chain: gather to rank 0's buffer, min there, scatter).
+void group_min(const std::vector<spark_ctx*>& m);
+
+void stage_launch(spark_ctx* c, const double* prev, const double* un, double a, double b, double* out,
+                  bool last, const double* dt_ptr, double dt_value, bool honor_active) {
+    spark::StageArgs A{};
+    A.g = c->plan.geo;
+    A.uprev = prev;
+    A.un = un;
+    A.uout = out;
+    for (int d = 0; d < 3; d++)
+        for (int s = 0; s < 2; s++) A.halo[d][s] = c->recv[d][s];
+    A.a = a;
+    A.b = b;
+    A.sc = c->sc;
+    A.dt_ptr = dt_ptr;
+    A.dt_value = dt_value;
+    A.last = last ? 1 : 0;
+    A.honor_active = honor_active ? 1 : 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->prof) {
+        if (c->ev_used == c->ev.size()) {
+            cudaEvent_t x, y;
+            CU(cudaEventCreate(&x));
+            CU(cudaEventCreate(&y));
+            c->ev.emplace_back(x, y);
+        }
+        e0 = c->ev[c->ev_used].first;
+        e1 = c->ev[c->ev_used].second;
+        c->ev_used++;
+        CU(cudaEventRecord(e0, c->stream));
+    }
+    launched(c, spark::launch_stage(A, c->cfg.recon, c->cfg.riemann, c->stream), "stage kernel");
+    c->stage_launches++;
+    if (c->prof) CU(cudaEventRecord(e1, c->stream));
+}
+
+void rk_coeffs(int S, int s, double* a, double* b) {
+    if (s == 1) {
+        *a = 0.0;
+        *b = 1.0;
+    } else if (S == 2) {
+        *a = 0.5;
+        *b = 0.5;
+    } else if (s == 2) {
+        *a = 0.75;
+        *b = 0.25;
+    } else {
+        *a = 1.0 / 3.0;
+        *b = 2.0 / 3.0;
+    }
+}
+
+// Buffer schedule: stage s reads prev, writes out; returns the new U^n index.
+// RK2: n->x, (x,n)->y, U^{n+1}=y.  RK3: n->x, (x,n)->y, (y,n)->x, U^{n+1}=x.
+int stage_buffers(int S, int n, int s, int* prev, int* out) {
+    const int x = (n + 1) % 3, y = (n + 2) % 3;
+    if (s == 1) {
+        *prev = n;
+        *out = x;
+    } else if (s == 2) {
+        *prev = x;
+        *out = y;
+    } else {
+        *prev = y;
+        *out = x;
+    }
+    return S == 2 ? y : x;
+}
+
+void sync_and_check(spark_ctx* c, bool rollback_on_error, int old_n) {
+    CU(cudaStreamSynchronize(c->stream));
+    spark::DevScalars h;
+    CU(cudaMemcpy(&h, c->sc, sizeof(h), cudaMemcpyDeviceToHost));
+    if (h.status & 1) {
+        if (rollback_on_error && old_n >= 0) {
+            c->n_idx = old_n;
+            h.t = h.t_prev;
+            h.steps -= 1;
+            h.acc = h.acc_prev;
+            h.status = 0;
+            CU(cudaMemcpy(c->sc, &h, sizeof(h), cudaMemcpyHostToDevice));
+            throw Error(SPARK_ERR_NONPHYSICAL, "non-physical state (rho<=0, p<=0 or NaN); rolled back to U^n");
+        }
+        throw Error(SPARK_ERR_NONPHYSICAL, "non-physical state (rho<=0, p<=0 or NaN)");
+    }
+}
+
+void do_step(spark_ctx* c, double dt) {
+    // single context (1 rank or NCCL); the caller set t_end through do_begin
+    const int S = c->cfg.rk_stages;
+    int newn = c->n_idx;
+    for (int s = 1; s <= S; s++) {
+        int pi, po;
+        newn = stage_buffers(S, c->n_idx, s, &pi, &po);
+        double a, b;
+        rk_coeffs(S, s, &a, &b);
+        if (c->nranks > 1) {
+            pack_all(c, c->U[pi]);
+            exchange_nccl(c);
+        }
+        stage_launch(c, c->U[pi], c->U[c->n_idx], a, b, c->U[po], s == S, &c->sc->dt, dt, true);
+    }
+    allreduce_acc(c);
+    c->n_idx = newn;
+}
+
+}  // namespace
+
+// ===================================================================== ABI
+extern "C" {
+
+int32_t spark_abi_version(void) { return SPARK_ABI_VERSION; }
+
+const char* spark_status_string(spark_status st) {
+    switch (st) {
+        case SPARK_OK: return "ok";
+        case SPARK_ERR_ARG: return "invalid argument";
+        case SPARK_ERR_CUDA: return "CUDA error";
+        case SPARK_ERR_NCCL: return "NCCL error";
+        case SPARK_ERR_OOM: return "arena too small";
+        case SPARK_ERR_NONPHYSICAL: return "non-physical state";
+        case SPARK_ERR_STATE: return "call out of order";
+    }
+    return "unknown status";
+}
+
+spark_status spark_check_config(const spark_config* cfg, int32_t nranks) {
+    std::string m = check(cfg, nranks);
+    if (!m.empty()) return SPARK_ERR_ARG;
+    int pg[3];
+    return rank_grid(cfg, nranks, pg) ? SPARK_OK : SPARK_ERR_ARG;
+}
+
+spark_status spark_rank_grid(const spark_config* cfg, int32_t nranks, int32_t pgrid[3]) {
+    return guard(nullptr, [&] {
+        Plan p = make_plan(cfg, 0, nranks);
+        for (int d = 0; d < 3; d++) pgrid[d] = p.pg[d];
+    });
+}
+
+spark_status spark_rank_box(const spark_config* cfg, int32_t rank, int32_t nranks, int32_t box_lo[3],
+                            int32_t box_n[3]) {
+    return guard(nullptr, [&] {
+        Plan p = make_plan(cfg, rank, nranks);
+        for (int d = 0; d < 3; d++) {
+            box_lo[d] = p.box_lo[d];
+            box_n[d] = p.box_n[d];
+        }
+    });
+}
+
+spark_status spark_halo_plan(const spark_config* cfg, int32_t rank, int32_t nranks, spark_face_plan faces[6],
+                             int32_t* nfaces) {
+    return guard(nullptr, [&] {
+        Plan p = make_plan(cfg, rank, nranks);
+        int n = 0;
+        for (int d = 0; d < cfg->ndim; d++)
+            for (int s = 0; s < 2; s++) {
+                faces[n].dim = d;
+                faces[n].side = s;
+                faces[n].peer = p.peer[d][s];
+                faces[n].pad = 0;
+                faces[n].cells = p.peer[d][s] >= 0 ? p.geo.slab[d] : 0;
+                n++;
+            }
+        *nfaces = n;
+    });
+}
+
+spark_status spark_required_bytes(const spark_config* cfg, int32_t rank, int32_t nranks, size_t* bytes) {
+    return guard(nullptr, [&] {
+        if (!bytes) throw Error(SPARK_ERR_ARG, "null bytes");
+        *bytes = arena_bytes(make_plan(cfg, rank, nranks));
+    });
+}
+
+spark_status spark_nccl_unique_id(uint8_t id[128]) {
+    return guard(nullptr, [&] {
+        ncclUniqueId u;
+        NC(ncclGetUniqueId(&u));
+        static_assert(sizeof(u) == 128, "nccl unique id size");
+        std::memcpy(id, &u, 128);
+    });
+}
+
+spark_status spark_init(const spark_config* cfg, int32_t rank, int32_t nranks, const uint8_t* nccl_id,
+                        int32_t device, void* cuda_stream, void* arena, size_t arena_bytes_, spark_ctx** out) {
+    if (!out) return SPARK_ERR_ARG;
+    *out = nullptr;
+    spark_ctx* made = nullptr;
+    spark_status st = guard(nullptr, [&] {
+        if (nranks > 1 && !nccl_id) throw Error(SPARK_ERR_ARG, "nranks > 1 needs an NCCL id");
+        std::unique_ptr<spark_ctx> c(make_ctx(cfg, rank, nranks, device, cuda_stream, arena, arena_bytes_));
+        if (nranks > 1) {
+            ncclUniqueId u;
+            std::memcpy(&u, nccl_id, 128);
+            NC(ncclCommInitRank(&c->comm, nranks, u, rank));
+        }
+        made = c.release();
+    });
+    *out = made;
+    return st;
+}
+
+spark_status spark_init_local_group(const spark_config* cfg, int32_t nranks, int32_t device, void* cuda_stream,
+                                    void* const* arenas, size_t arena_bytes_, spark_ctx** outs) {
+    if (!outs || !arenas) return SPARK_ERR_ARG;
+    std::vector<spark_ctx*> made;
+    spark_status st = guard(nullptr, [&] {
+        auto grp = std::make_shared<LocalGroup>();
+        for (int r = 0; r < nranks; r++) {
+            spark_ctx* c = make_ctx(cfg, r, nranks, device, cuda_stream, arenas[r], arena_bytes_);
+            c->group = grp;
+            made.push_back(c);
+            grp->members.push_back(c);
+        }
+    });
+    if (st != SPARK_OK) {
+        for (auto* c : made) delete c;
+        return st;
+    }
+    for (int r = 0; r < nranks; r++) outs[r] = made[r];
+    return SPARK_OK;
+}
+
+spark_status spark_finalize(spark_ctx* ctx) {
+    if (!ctx) return SPARK_ERR_ARG;
+    spark_status st = guard(ctx, [&] {
+        set_device(ctx);
+        CU(cudaStreamSynchronize(ctx->stream));
+        for (auto& e : ctx->ev) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+        if (ctx->comm) ncclCommDestroy(ctx->comm);
+    });
+    if (ctx->group) {
+        auto& m = ctx->group->members;
+        m.erase(std::remove(m.begin(), m.end(), ctx), m.end());
+    }
+    delete ctx;
+    return st;
+}
+
+const char* spark_last_error(const spark_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+static void after_state_loaded(spark_ctx* c) {
+    launched(c, spark::launch_scalars_reset(c->sc, c->stream), "scalars reset");
+    launched(c, spark::launch_cfl_min(c->plan.geo, c->U[c->n_idx], c->sc, c->stream), "cfl min");
+    allreduce_acc(c);
+    c->have_state = true;
+}
+
+spark_status spark_set_state(spark_ctx* ctx, const double* U, int32_t on_device) {
+    if (!ctx || !U) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        set_device(ctx);
+        const size_t bytes = sizeof(double) * ctx->plan.geo.nvar * (size_t)ctx->plan.geo.ncell;
+        ctx->n_idx = 0;
+        CU(cudaMemcpyAsync(ctx->U[0], U, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           ctx->stream));
+        after_state_loaded(ctx);
+    });
+}
+
+spark_status spark_set_primitive(spark_ctx* ctx, const double* W, int32_t on_device) {
+    if (!ctx || !W) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        set_device(ctx);
+        const size_t bytes = sizeof(double) * ctx->plan.geo.nvar * (size_t)ctx->plan.geo.ncell;
+        ctx->n_idx = 0;
+        const double* src = W;
+        if (!on_device) {  // stage through U[1] (dead before the first step)
+            CU(cudaMemcpyAsync(ctx->U[1], W, bytes, cudaMemcpyHostToDevice, ctx->stream));
+            src = ctx->U[1];
+        }
+        launched(ctx, spark::launch_prim_to_cons(ctx->plan.geo, src, ctx->U[0], ctx->stream), "prim to cons");
+        after_state_loaded(ctx);
+    });
+}
+
+spark_status spark_get_state(spark_ctx* ctx, double* U, int32_t on_device) {
+    if (!ctx || !U) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        if (!ctx->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
+        set_device(ctx);
+        const size_t bytes = sizeof(double) * ctx->plan.geo.nvar * (size_t)ctx->plan.geo.ncell;
+        CU(cudaMemcpyAsync(U, ctx->U[ctx->n_idx], bytes,
+                           on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+        sync_and_check(ctx, false, -1);
+    });
+}
+
+spark_status spark_get_time(spark_ctx* ctx, double* t, int64_t* steps, double* dt_last) {
+    if (!ctx) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        set_device(ctx);
+        CU(cudaStreamSynchronize(ctx->stream));
+        spark::DevScalars h;
+        CU(cudaMemcpy(&h, ctx->sc, sizeof(h), cudaMemcpyDeviceToHost));
+        if (t) *t = h.t;
+        if (steps) *steps = h.steps;
+        if (dt_last) *dt_last = h.dt;
+    });
+}
+
+spark_status spark_get_cfl_min(spark_ctx* ctx, double* value) {
+    if (!ctx || !value) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        if (!ctx->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
+        set_device(ctx);
+        CU(cudaStreamSynchronize(ctx->stream));
+        spark::DevScalars h;
+        CU(cudaMemcpy(&h, ctx->sc, sizeof(h), cudaMemcpyDeviceToHost));
+        long long bits = (long long)h.acc;
+        std::memcpy(value, &bits, sizeof(double));
+    });
+}
+
+spark_status spark_fill_guardcells(spark_ctx* ctx, double* padded_out) {
+    if (!ctx) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        if (!ctx->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
+        set_device(ctx);
+        if (ctx->group) {
+            for (spark_ctx* m : ctx->group->members) pack_all(m, m->U[m->n_idx]);
+            exchange_local(ctx->group->members);
+        } else if (ctx->nranks > 1) {
+            pack_all(ctx, ctx->U[ctx->n_idx]);
+            exchange_nccl(ctx);
+        }
+        if (padded_out) {
+            const double* halo[3][2];
+            for (int d = 0; d < 3; d++)
+                for (int s = 0; s < 2; s++) halo[d][s] = ctx->recv[d][s];
+            launched(ctx, spark::launch_fill_padded(ctx->plan.geo, ctx->U[ctx->n_idx], halo, padded_out, ctx->stream),
+                     "fill padded");
+        }
+    });
+}
+
+spark_status spark_step(spark_ctx* ctx, double dt, double t_end, double* dt_used) {
+    if (!ctx) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        if (!ctx->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
+        if (ctx->group) throw Error(SPARK_ERR_STATE, "local-group contexts step with spark_step_group");
+        set_device(ctx);
+        const int old_n = ctx->n_idx;
+        launched(ctx, spark::launch_step_begin(ctx->sc, dt, t_end, ctx->cfg.cfl, ctx->stream), "step begin");
+        do_step(ctx, dt);
+        if (dt_used) {
+            sync_and_check(ctx, true, old_n);
+            double h;
+            CU(cudaMemcpy(&h, &ctx->sc->dt, sizeof(double), cudaMemcpyDeviceToHost));
+            *dt_used = h;
+        }
+    });
+}
+
+spark_status spark_advance(spark_ctx* ctx, int64_t max_steps, double t_end, int32_t check_every,
+                           int64_t* steps_done) {
+    if (!ctx) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        if (!ctx->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
+        if (ctx->group) throw Error(SPARK_ERR_STATE, "local-group contexts step with spark_step_group");
+        set_device(ctx);
+        spark::DevScalars h0;
+        CU(cudaStreamSynchronize(ctx->stream));
+        CU(cudaMemcpy(&h0, ctx->sc, sizeof(h0), cudaMemcpyDeviceToHost));
+        for (int64_t n = 0; n < max_steps; n++) {
+            launched(ctx, spark::launch_step_begin(ctx->sc, 0.0, t_end, ctx->cfg.cfl, ctx->stream), "step begin");
+            do_step(ctx, 0.0);
+            if ((check_every > 0 && (n + 1) % check_every == 0) || n + 1 == max_steps) {
+                sync_and_check(ctx, false, -1);
+                spark::DevScalars h;
+                CU(cudaMemcpy(&h, ctx->sc, sizeof(h), cudaMemcpyDeviceToHost));
+                if (!h.active || (t_end > 0.0 && h.t >= t_end * (1.0 - 1e-14))) break;
+            }
+        }
+        sync_and_check(ctx, false, -1);
+        spark::DevScalars h;
+        CU(cudaMemcpy(&h, ctx->sc, sizeof(h), cudaMemcpyDeviceToHost));
+        if (steps_done) *steps_done = h.steps - h0.steps;
+    });
+}
+
+spark_status spark_step_group(spark_ctx* const* ctxs, int32_t n, double dt, double t_end, double* dt_used) {
+    if (!ctxs || n < 1 || !ctxs[0]) return SPARK_ERR_ARG;
+    spark_ctx* c0 = ctxs[0];
+    return guard(c0, [&] {
+        if (!c0->group || (int)c0->group->members.size() != n)
+            throw Error(SPARK_ERR_ARG, "spark_step_group needs all contexts of one local group");
+        std::vector<spark_ctx*> m(c0->group->members);
+        for (spark_ctx* c : m)
+            if (!c->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
+        set_device(c0);
+        group_min(m);  // global CFL minimum of U^n (set_state computes it per rank)
+        std::vector<int> old(n);
+        for (int r = 0; r < n; r++) {
+            old[r] = m[r]->n_idx;
+            launched(m[r], spark::launch_step_begin(m[r]->sc, dt, t_end, m[r]->cfg.cfl, m[r]->stream), "step begin");
+        }
+        const int S = c0->cfg.rk_stages;
+        for (int s = 1; s <= S; s++) {
+            for (spark_ctx* c : m) {
+                int pi, po;
+                stage_buffers(S, c->n_idx, s, &pi, &po);
+                pack_all(c, c->U[pi]);
+            }
+            exchange_local(m);
+            for (spark_ctx* c : m) {
+                int pi, po;
+                stage_buffers(S, c->n_idx, s, &pi, &po);
+                double a, b;
+                rk_coeffs(S, s, &a, &b);
+                stage_launch(c, c->U[pi], c->U[c->n_idx], a, b, c->U[po], s == S, &c->sc->dt, dt, true);
+            }
+        }
+        group_min(m);
+        for (spark_ctx* c : m) {
+            int pi, po;
+            c->n_idx = stage_buffers(S, c->n_idx, 1, &pi, &po);
+        }
+        if (dt_used) {
+            for (int r = 0; r < n; r++) sync_and_check(m[r], true, old[r]);
+            double h;
+            CU(cudaMemcpy(&h, &c0->sc->dt, sizeof(double), cudaMemcpyDeviceToHost));
+            *dt_used = h;
+        }
+    });
+}
+
+spark_status spark_stage_apply(spark_ctx* ctx, const double* U_prev, const double* U_n, double a, double b, double dt,
+                               double* U_out) {
+    if (!ctx || !U_prev || !U_out) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        if (ctx->nranks != 1) throw Error(SPARK_ERR_STATE, "spark_stage_apply needs a single-rank context");
+        if (a != 0.0 && !U_n) throw Error(SPARK_ERR_ARG, "U_n required when a != 0");
+        set_device(ctx);
+        stage_launch(ctx, U_prev, U_n, a, b, U_out, false, nullptr, dt, false);
+    });
+}
+
+spark_status spark_profile_enable(spark_ctx* ctx, int32_t on) {
+    if (!ctx) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        ctx->prof = on != 0;
+        if (on) {
+            ctx->ev_used = 0;
+            ctx->stage_launches = 0;
+            ctx->total_launches = 0;
+            ctx->prof_ms = 0.0;
+        }
+    });
+}
+
+spark_status spark_profile_read(spark_ctx* ctx, double* stage_ms, int64_t* stage_launches, int64_t* total_launches) {
+    if (!ctx) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        set_device(ctx);
+        CU(cudaStreamSynchronize(ctx->stream));
+        double ms = 0.0;
+        for (size_t i = 0; i < ctx->ev_used; i++) {
+            float x = 0.f;
+            CU(cudaEventElapsedTime(&x, ctx->ev[i].first, ctx->ev[i].second));
+            ms += x;
+        }
+        if (stage_ms) *stage_ms = ms;
+        if (stage_launches) *stage_launches = ctx->stage_launches;
+        if (total_launches) *total_launches = ctx->total_launches;
+    });
+}
+
+}  // extern "C"
+
+namespace {
+// Local-group dt minimum: one tiny kernel takes the min of every member's
+// accumulator and writes it back to each (all members share one stream).
+void group_min(const std::vector<spark_ctx*>& m) {
+    if (m.size() > (size_t)spark::kMaxGroup) throw Error(SPARK_ERR_ARG, "local group too large");
+    spark::AccPtrs p{};
+    for (size_t r = 0; r < m.size(); r++) p.p[r] = &m[r]->sc->acc;
+    launched(m[0], spark::launch_group_min(p, (int)m.size(), m[0]->stream), "group min");
+}
+}  // namespace

@@ -1,0 +1,75 @@
+// spark_internal.h — types shared by the host layer (spark_api.cpp) and the
+// CUDA kernels (spark_kernels.cu).  Not part of the public ABI (include/spark.h).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace spark {
+
+constexpr int kMaxThreads = 1024;
+
+// Device-resident scalars of one context (one per rank).
+struct DevScalars {
+    double dt;                    // dt of the step in flight
+    double t;                     // time at the end of the step in flight
+    double t_prev;                // time at its start (rollback)
+    unsigned long long acc;       // CFL min accumulator: bits of a positive double
+    unsigned long long acc_prev;  // value consumed by the step in flight (rollback)
+    int status;                   // bit 0: non-physical state seen
+    int active;                   // 0 once t >= t_end: stages copy U unchanged
+    long long steps;              // completed steps
+    double pad[8];
+};
+
+// Geometry of this rank's sub-box, in cells.  Loaded by value into kernels.
+struct Geo {
+    int ndim, nvar, ng;           // ng = guard depth of the halo slabs
+    int nb[3];                    // cells per block
+    int bn[3];                    // blocks of the sub-box per dim
+    int cn[3];                    // cells of the sub-box per dim (nb * bn)
+    int gN[3];                    // global cells per dim
+    int off[3];                   // global cell index of the sub-box origin
+    int bc[3][2];                 // physical boundary conditions
+    int halo[3][2];               // 1: face neighbour is another rank (slab buffer)
+    long long ncell;              // cells of the sub-box (stride between variables)
+    long long cpb;                // cells per block
+    long long slab[3];            // cells of one slab of dim d (ng * other extents)
+    double dx[3], rdx[3];
+    double gamma, cfl;
+};
+
+struct StageArgs {
+    Geo g;
+    const double* uprev;
+    const double* un;             // may be null when a == 0
+    double* uout;
+    const double* halo[3][2];     // received slabs [v][slab] (null if no peer)
+    double a, b;
+    DevScalars* sc;
+    const double* dt_ptr;         // device dt (sc->dt) or null -> dt_value
+    double dt_value;
+    int last;                     // 1: fuse the CFL-min epilogue
+    int honor_active;             // 1: copy-through when sc->active == 0
+};
+
+constexpr int kMaxGroup = 64;
+struct AccPtrs {
+    unsigned long long* p[kMaxGroup];
+};
+
+// ---- launchers (spark_kernels.cu) -------------------------------------------
+// All return cudaGetLastError() after the launch.
+cudaError_t launch_stage(const StageArgs& a, int recon, int riemann, cudaStream_t s);
+cudaError_t launch_cfl_min(const Geo& g, const double* u, DevScalars* sc, cudaStream_t s);
+cudaError_t launch_step_begin(DevScalars* sc, double dt_fixed, double t_end, double cfl, cudaStream_t s);
+cudaError_t launch_prim_to_cons(const Geo& g, const double* w, double* u, cudaStream_t s);
+cudaError_t launch_pack(const Geo& g, const double* u, int dim, int side, double* slab, cudaStream_t s);
+cudaError_t launch_fill_padded(const Geo& g, const double* u, const double* const halo[3][2], double* padded,
+                               cudaStream_t s);
+cudaError_t launch_scalars_reset(DevScalars* sc, cudaStream_t s);
+cudaError_t launch_group_min(const AccPtrs& p, int n, cudaStream_t s);
+size_t stage_smem_bytes(const Geo& g, int recon);
+int stage_block_threads(const Geo& g);
+
+}  // namespace spark

@@ -117,24 +117,29 @@ def from_global(p: Problem, G: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(G.transpose(0, 1, 3, 5, 2, 4, 6).reshape(nv, nbz * nby * nbx, nk, nj, ni))
 
 
-def centres(p: Problem):
-    """Cell-centre coordinates (x, y, z) as global [Z][Y][X] arrays."""
+def centres(p: Problem, box=None):
+    """Cell-centre coordinates (x, y, z) as [Z][Y][X] arrays of the whole grid, or
+    of the sub-box ``box = ((lo_x, lo_y, lo_z), (n_x, n_y, n_z))`` in cells."""
     n = [p.nblk[d] * p.nb[d] for d in range(3)]
+    lo_c, n_c = box if box is not None else ((0, 0, 0), n)
     ax = []
     for d in range(3):
         h = (p.hi[d] - p.lo[d]) / n[d]
-        ax.append(p.lo[d] + (np.arange(n[d]) + 0.5) * h)
+        ax.append(p.lo[d] + (np.arange(lo_c[d], lo_c[d] + n_c[d]) + 0.5) * h)
     z, y, x = np.meshgrid(ax[2], ax[1], ax[0], indexing="ij")
     return x, y, z
 
 
-def _prim_global(p: Problem, rho, vel, pres) -> np.ndarray:
+def _prim_global(p: Problem, rho, vel, pres, box=None) -> np.ndarray:
     shape = rho.shape
     W = np.zeros((p.nvar,) + shape, dtype=np.float64)
     W[0] = rho
     for d in range(p.ndim):
         W[1 + d] = vel[d] if vel is not None else 0.0
     W[p.ndim + 1] = pres
+    if box is not None:  # canonical layout of the sub-box (its own block grid)
+        q = replace(p, nblk=tuple(box[1][d] // p.nb[d] for d in range(3)))
+        return from_global(q, W)
     return from_global(p, W)
 
 
@@ -157,12 +162,13 @@ def sod_square(p: Problem) -> np.ndarray:
     return _prim_global(p, rho, None, pres)
 
 
-def sedov(p: Problem, e_blast: float = 1.0, p_amb: float = 1e-5, r0_cells: float = 3.5) -> np.ndarray:
+def sedov(p: Problem, e_blast: float = 1.0, p_amb: float = 1e-5, r0_cells: float = 3.5, box=None) -> np.ndarray:
     """Sedov blast: E_blast deposited as uniform internal energy within r0 of the centre.
 
     p_dep = (gamma-1) E_blast / (n_dep dV) is the IC's definition of the deposit
-    (an input recipe, not the method's EOS)."""
-    x, y, z = centres(p)
+    (an input recipe, not the method's EOS).  ``box`` (cells) restricts the
+    output to one rank's sub-box; n_dep is always counted on the whole grid."""
+    x, y, z = centres(p, box)
     dxs = [(p.hi[d] - p.lo[d]) / (p.nblk[d] * p.nb[d]) for d in range(3)]
     c = [0.5 * (p.lo[d] + p.hi[d]) for d in range(3)]
     r2 = (x - c[0]) ** 2
@@ -172,12 +178,28 @@ def sedov(p: Problem, e_blast: float = 1.0, p_amb: float = 1e-5, r0_cells: float
         r2 = r2 + (z - c[2]) ** 2
     r0 = r0_cells * dxs[0]
     dep = r2 < r0 * r0
-    n_dep = int(dep.sum())
+    n_dep = _sedov_ndep(p, r0) if box is not None else int(dep.sum())
     dV = float(np.prod(dxs[: p.ndim]))
     rho = np.ones_like(x)
     pres = np.full_like(x, p_amb)
     pres[dep] = (p.gamma - 1.0) * e_blast / (n_dep * dV)
-    return _prim_global(p, rho, None, pres)
+    return _prim_global(p, rho, None, pres, box)
+
+
+def _sedov_ndep(p: Problem, r0: float) -> int:
+    """Number of deposit cells on the whole grid (only the neighbourhood of the centre)."""
+    n = [p.nblk[d] * p.nb[d] for d in range(3)]
+    k = int(np.ceil(r0 / ((p.hi[0] - p.lo[0]) / n[0]))) + 2
+    lo = [max(0, n[d] // 2 - k) if d < p.ndim else 0 for d in range(3)]
+    hi = [min(n[d], n[d] // 2 + k) if d < p.ndim else 1 for d in range(3)]
+    x, y, z = centres(p, (tuple(lo), tuple(hi[d] - lo[d] for d in range(3))))
+    c = [0.5 * (p.lo[d] + p.hi[d]) for d in range(3)]
+    r2 = (x - c[0]) ** 2
+    if p.ndim >= 2:
+        r2 = r2 + (y - c[1]) ** 2
+    if p.ndim >= 3:
+        r2 = r2 + (z - c[2]) ** 2
+    return int((r2 < r0 * r0).sum())
 
 
 def random_state(p: Problem, seed: int, blocky: bool = False) -> np.ndarray:
@@ -237,13 +259,14 @@ def index_encoded(p: Problem) -> np.ndarray:
     return from_global(p, G)
 
 
-def initial_primitive(p: Problem, seed: int = 0) -> np.ndarray:
+def initial_primitive(p: Problem, seed: int = 0, box=None) -> np.ndarray:
+    if p.ic == "sedov":
+        return sedov(p, box=box)
+    assert box is None, "sub-box generation only for sedov"
     if p.ic == "sod_x":
         return sod_x(p)
     if p.ic == "sod_square":
         return sod_square(p)
-    if p.ic == "sedov":
-        return sedov(p)
     if p.ic == "random":
         return random_state(p, seed)
     if p.ic == "blocky":
