@@ -221,6 +221,16 @@ spark_status spark_profile_enable(spark_ctx* ctx, int32_t on);
 spark_status spark_profile_read(spark_ctx* ctx, double* stage_ms, int64_t* stage_launches,
                                 int64_t* total_launches);
 
+/* ---- self test ----------------------------------------------------------------- */
+
+/* Evaluate the device Riemann solver (the one KB1 calls, calcFlux P:1833) on n
+ * face states given in HOST memory, unrotated primitive order (rho, u_1..u_ndim,
+ * p), arrays [n][ndim+2]; normal direction dir (0..ndim-1); riemann as
+ * spark_riemann.  f (host, [n][ndim+2]) receives the conserved fluxes.
+ * Synchronises (device 'device', default stream).  For tests. */
+spark_status spark_selftest_riemann(int32_t device, int32_t riemann, int32_t ndim, int32_t dir, double gamma,
+                                    int64_t n, const double* wl, const double* wr, double* f);
+
 #ifdef __cplusplus
 }
 #endif

@@ -818,3 +818,30 @@ void group_min(const std::vector<spark_ctx*>& m) {
     launched(m[0], spark::launch_group_min(p, (int)m.size(), m[0]->stream), "group min");
 }
 }  // namespace
+
+extern "C" spark_status spark_selftest_riemann(int32_t device, int32_t riemann, int32_t ndim, int32_t dir,
+                                               double gamma, int64_t n, const double* wl, const double* wr,
+                                               double* f) {
+    return guard(nullptr, [&] {
+        if (ndim < 1 || ndim > 3 || dir < 0 || dir >= ndim || n < 0 || !wl || !wr || !f || riemann < 0 ||
+            riemann > 1)
+            throw Error(SPARK_ERR_ARG, "bad selftest arguments");
+        CU(cudaSetDevice(device));
+        const size_t bytes = sizeof(double) * (size_t)n * (ndim + 2);
+        double* d = nullptr;
+        CU(cudaMalloc(&d, 3 * bytes + 8));
+        struct Free {
+            double* p;
+            ~Free() { cudaFree(p); }
+        } fr{d};
+        char* base = reinterpret_cast<char*>(d);
+        double* dl = d;
+        double* dr = reinterpret_cast<double*>(base + bytes);
+        double* df = reinterpret_cast<double*>(base + 2 * bytes);
+        CU(cudaMemcpy(dl, wl, bytes, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(dr, wr, bytes, cudaMemcpyHostToDevice));
+        if (n > 0) CU(spark::launch_selftest_riemann(riemann, ndim, dir, gamma, n, dl, dr, df));
+        CU(cudaDeviceSynchronize());
+        CU(cudaMemcpy(f, df, bytes, cudaMemcpyDeviceToHost));
+    });
+}

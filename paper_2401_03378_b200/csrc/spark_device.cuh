@@ -1,0 +1,328 @@
+// spark_device.cuh — device helpers of the Spark hot path (sm_100a, FP64).
+//
+// EOS, reconstruction, Riemann solvers and the guard-cell gather shared by the
+// kernels.  The paper prints no formulas; these are the textbook readings of
+// DESIGN.md §3 (ideal gas; PLM-minmod / WENO5-JS on primitive variables with a
+// first-order positivity fallback; HLL / HLLC with Davis wave speeds, Toro §10.4).
+// Formulations are chosen for the FP64 issue budget of B200:
+// reciprocals and square roots are one MUFU seed plus one cubic Newton step
+// (<= 1 ulp from the correctly rounded value, no slow-path branches), the
+// minmod limiter and the positivity tests run on the integer pipe, and the
+// reconstruction is cell-centric (one limiter / smoothness evaluation per cell
+// and direction, shared by the cell's two faces).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+
+#include "spark_internal.h"
+
+namespace spark {
+namespace dev {
+
+constexpr int BC_PERIODIC = 0, BC_OUTFLOW = 1;  // BC_REFLECT = 2
+
+template <int RECON>
+struct StencilOf {
+    static constexpr int NG = RECON == 2 ? 3 : (RECON == 1 ? 2 : 1);  // cells each side of a face
+};
+
+// ------------------------------------------------------------ arithmetic
+// 1/x: MUFU seed (~2^-22) and one cubic Newton step y(1 + e + e^2), e = 1 - xy.
+__host__ __device__ __forceinline__ double rcp(double x) {
+#ifdef __CUDA_ARCH__
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = __hiloint2double(__double2hiint(y), 0);  // MUFU.RCP64H writes the high word only
+#else
+    double y = (double)(1.0f / (float)x);  // host build (tests): same Newton step from an fp32 seed
+#endif
+    const double e = fma(-x, y, 1.0);
+    return fma(y, fma(e, e, e), y);
+}
+
+// sqrt(a), a > 0: h = a y with y ~ 1/sqrt(a), then h(1 + r/2 + 3r^2/8), r = 1 - a y^2.
+__host__ __device__ __forceinline__ double sqrt_fast(double a) {
+#ifdef __CUDA_ARCH__
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    y = __hiloint2double(__double2hiint(y), 0);  // MUFU.RSQ64H writes the high word only
+#else
+    double y = (double)(1.0f / sqrtf((float)a));
+#endif
+    const double h = a * y;
+    const double r = fma(-h, y, 1.0);
+    return fma(h * r, fma(0.375, r, 0.5), h);
+}
+
+// x > 0 for non-NaN x, on the integer pipe (+0 and -0 are not positive).
+__host__ __device__ __forceinline__ long long dbits(double x) {
+#ifdef __CUDA_ARCH__
+    return __double_as_longlong(x);
+#else
+    long long b;
+    __builtin_memcpy(&b, &x, 8);
+    return b;
+#endif
+}
+
+__host__ __device__ __forceinline__ bool positive(double x) { return dbits(x) > 0; }
+
+// minmod(a, b): 0 unless a and b are both nonzero with the same sign, else the
+// one of smaller magnitude (ties: b).  Integer pipe only; bitwise equal to
+// the oracle's comparison form (reading R2).
+__host__ __device__ __forceinline__ double minmod(double a, double b) {
+    const long long ia = dbits(a), ib = dbits(b);
+    const unsigned long long ma = (unsigned long long)ia & 0x7fffffffffffffffull;
+    const unsigned long long mb = (unsigned long long)ib & 0x7fffffffffffffffull;
+    const bool keep = ((ia ^ ib) >= 0) && ma != 0 && mb != 0;
+    const double r = ma < mb ? a : b;
+    return keep ? r : 0.0;
+}
+
+// ------------------------------------------------------------------- EOS
+// Ideal gas (EOS unit): u = m/rho, p = (gamma-1)(E - m.u/2).
+// Returns false for rho <= 0, p <= 0 or non-finite p (calcEos check).
+template <int NV>
+__host__ __device__ __forceinline__ bool cons_to_prim(const double* u, double* w, double gm1) {
+    const double rho = u[0];
+    const double inv = rcp(rho);
+    double ke = 0.0;
+#pragma unroll
+    for (int d = 1; d < NV - 1; d++) {
+        w[d] = u[d] * inv;
+        ke = fma(u[d], w[d], ke);
+    }
+    w[0] = rho;
+    const double p = gm1 * fma(-0.5, ke, u[NV - 1]);
+    w[NV - 1] = p;
+    return rho > 0.0 && p > 0.0 && p < INFINITY;
+}
+
+// -------------------------------------------------------- reconstruction
+// Cell-centric reconstruction of one variable: from s[0..2R] = W_{i-R..i+R}
+// the values at the left (lo, face i-1/2) and right (hi, face i+1/2) edges.
+template <int RECON>
+__host__ __device__ __forceinline__ void recon_cell(const double* s, double& lo, double& hi) {
+    if (RECON == 0) {
+        lo = hi = s[0];
+    } else if (RECON == 1) {  // PLM-minmod
+        const double d = minmod(s[1] - s[0], s[2] - s[1]);
+        lo = fma(-0.5, d, s[1]);
+        hi = fma(0.5, d, s[1]);
+    } else {  // WENO5-JS, both edges from shared smoothness indicators
+        const double a = s[0], b = s[1], c = s[2], d = s[3], e = s[4];
+        const double eps = 1e-6;
+        const double t0 = a - 2.0 * b + c, u0 = a - 4.0 * b + 3.0 * c;
+        const double t1 = b - 2.0 * c + d, u1 = b - d;
+        const double t2 = c - 2.0 * d + e, u2 = 3.0 * c - 4.0 * d + e;
+        const double b0 = fma(13.0 / 12.0 * t0, t0, 0.25 * u0 * u0);
+        const double b1 = fma(13.0 / 12.0 * t1, t1, 0.25 * u1 * u1);
+        const double b2 = fma(13.0 / 12.0 * t2, t2, 0.25 * u2 * u2);
+        const double e0 = eps + b0, e1 = eps + b1, e2 = eps + b2;
+        const double s0 = e0 * e0, s1 = e1 * e1, s2 = e2 * e2;
+        // alpha_k = d_k / s_k ; multiply through by s0 s1 s2 (one reciprocal per edge)
+        const double P0 = s1 * s2, P1 = s0 * s2, P2 = s0 * s1;
+        constexpr double k6 = 1.0 / 6.0;
+        // right edge (i+1/2): linear weights (0.1, 0.6, 0.3) on stencils (a,b,c), (b,c,d), (c,d,e)
+        const double q0 = (2.0 * a - 7.0 * b + 11.0 * c) * k6;
+        const double q1 = (-b + 5.0 * c + 2.0 * d) * k6;
+        const double q2 = (2.0 * c + 5.0 * d - e) * k6;
+        const double w0 = 0.1 * P0, w1 = 0.6 * P1, w2 = 0.3 * P2;
+        hi = fma(w0, q0, fma(w1, q1, w2 * q2)) * rcp(w0 + w1 + w2);
+        // left edge (i-1/2): the mirrored stencil, weights (0.1, 0.6, 0.3) on (e,d,c), (d,c,b), (c,b,a)
+        const double r0 = (2.0 * e - 7.0 * d + 11.0 * c) * k6;
+        const double r1 = (-d + 5.0 * c + 2.0 * b) * k6;
+        const double r2 = (2.0 * c + 5.0 * b - a) * k6;
+        const double v0 = 0.1 * P2, v1 = 0.6 * P1, v2 = 0.3 * P0;
+        lo = fma(v0, r0, fma(v1, r1, v2 * r2)) * rcp(v0 + v1 + v2);
+    }
+}
+
+// ------------------------------------------------------------- Riemann
+// HLL / HLLC (Toro §10.4), Davis wave speeds.  States and flux in the
+// unrotated primitive / conserved order; D is the face normal.  HLLC evaluates
+// only the state K whose flux is selected.
+template <int NV, int RS, int D>
+__host__ __device__ __forceinline__ void riemann(const double* wl, const double* wr, double gamma, double gm1i,
+                                        double* f) {
+    constexpr int N = 1 + D;
+    const double rl = wl[0], ul = wl[N], pl = wl[NV - 1];
+    const double rr = wr[0], ur = wr[N], pr = wr[NV - 1];
+    const double irl = rcp(rl), irr = rcp(rr);
+    const double cl = sqrt_fast(gamma * pl * irl), cr = sqrt_fast(gamma * pr * irr);
+    const double sl = fmin(ul - cl, ur - cr);
+    const double sr = fmax(ul + cl, ur + cr);
+    if (RS == 1) {
+        const double ql = rl * (sl - ul), qr = rr * (sr - ur);  // rho_K (S_K - u_K)
+        const double sstar = (pr - pl + ul * ql - ur * qr) * rcp(ql - qr);
+        const bool lpos = sl >= 0.0, rneg = sr <= 0.0;
+        const bool left = lpos || (!rneg && sstar >= 0.0);
+        // every K-side quantity selected at one place
+        double w[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) w[v] = left ? wl[v] : wr[v];
+        const double sk = left ? sl : sr, qk = left ? ql : qr, irho = left ? irl : irr;
+        const double rho = w[0], un = w[N], p = w[NV - 1];
+        double u2 = 0.0;
+#pragma unroll
+        for (int d = 1; d < NV - 1; d++) u2 = fma(w[d], w[d], u2);
+        const double E = fma(0.5 * rho, u2, p * gm1i);
+        const double mflux = rho * un;
+        f[0] = mflux;
+#pragma unroll
+        for (int d = 1; d < NV - 1; d++) f[d] = mflux * w[d];
+        f[N] += p;
+        f[NV - 1] = un * (E + p);
+        if (!lpos && !rneg) {
+            const double fac = qk * rcp(sk - sstar);
+            const double es = fma(sstar - un, fma(p, rcp(qk), sstar), E * irho);
+            f[0] = fma(sk, fac - rho, f[0]);
+#pragma unroll
+            for (int d = 1; d < NV - 1; d++) f[d] = fma(sk, fma(fac, d == N ? sstar : w[d], -rho * w[d]), f[d]);
+            f[NV - 1] = fma(sk, fma(fac, es, -E), f[NV - 1]);
+        }
+    } else {
+        double u2l = 0.0, u2r = 0.0;
+#pragma unroll
+        for (int d = 1; d < NV - 1; d++) {
+            u2l = fma(wl[d], wl[d], u2l);
+            u2r = fma(wr[d], wr[d], u2r);
+        }
+        const double El = fma(0.5 * rl, u2l, pl * gm1i), Er = fma(0.5 * rr, u2r, pr * gm1i);
+        const double ml = rl * ul, mr = rr * ur;
+        double UL[NV], UR[NV], FL[NV], FR[NV];
+        UL[0] = rl;
+        UR[0] = rr;
+        FL[0] = ml;
+        FR[0] = mr;
+#pragma unroll
+        for (int d = 1; d < NV - 1; d++) {
+            UL[d] = rl * wl[d];
+            UR[d] = rr * wr[d];
+            FL[d] = ml * wl[d];
+            FR[d] = mr * wr[d];
+        }
+        FL[N] += pl;
+        FR[N] += pr;
+        UL[NV - 1] = El;
+        UR[NV - 1] = Er;
+        FL[NV - 1] = ul * (El + pl);
+        FR[NV - 1] = ur * (Er + pr);
+        if (sl >= 0.0) {
+#pragma unroll
+            for (int v = 0; v < NV; v++) f[v] = FL[v];
+        } else if (sr <= 0.0) {
+#pragma unroll
+            for (int v = 0; v < NV; v++) f[v] = FR[v];
+        } else {
+            const double inv = rcp(sr - sl), slsr = sl * sr;
+#pragma unroll
+            for (int v = 0; v < NV; v++) f[v] = fma(slsr, UR[v] - UL[v], sr * FL[v] - sl * FR[v]) * inv;
+        }
+    }
+}
+
+// ------------------------------------------------------------ guard gather
+// Conserved values of the cell at sub-box coordinates l (may lie up to ng
+// cells outside the sub-box).  Out-of-box coordinates are resolved per
+// dimension: a face with a peer rank reads the received slab, otherwise the
+// physical boundary map (periodic wrap / outflow clamp / reflect mirror with
+// the normal momentum negated).  Returns false (out unset) when the cell lies
+// outside the sub-box in two or more peer directions (an edge or corner owned
+// by a diagonal rank; never needed by the star stencil).
+template <int NV>
+__device__ __forceinline__ bool fetch_cons(const Geo& g, const double* __restrict__ u,
+                                           const double* const (&halo)[3][2], int l0, int l1, int l2,
+                                           double* out) {
+    int l[3] = {l0, l1, l2};
+    bool flip[3] = {false, false, false};
+    int hd = -1, hs = 0;
+#pragma unroll
+    for (int d = 0; d < 3; d++) {
+        if (d >= g.ndim) continue;
+        const int x = l[d];
+        if (x < 0 || x >= g.cn[d]) {
+            const int side = x >= g.cn[d] ? 1 : 0;
+            if (g.halo[d][side]) {
+                if (hd >= 0) return false;
+                hd = d;
+                hs = side;
+            } else {
+                const int N = g.gN[d];
+                int gx = g.off[d] + x;
+                const int bc = g.bc[d][side];
+                if (bc == BC_PERIODIC) {
+                    gx %= N;
+                    if (gx < 0) gx += N;
+                } else if (bc == BC_OUTFLOW) {
+                    gx = side ? N - 1 : 0;
+                } else {
+                    gx = side ? 2 * N - 1 - gx : -1 - gx;
+                    flip[d] = true;
+                }
+                l[d] = gx - g.off[d];
+            }
+        }
+    }
+    const double* base;
+    long long idx, stride;
+    if (hd >= 0) {
+        int c[3] = {l[0], l[1], l[2]};
+        c[hd] = hs ? l[hd] - g.cn[hd] : l[hd] + g.ng;
+        const int e0 = hd == 0 ? g.ng : g.cn[0];
+        const int e1 = hd == 1 ? g.ng : g.cn[1];
+        idx = ((long long)c[2] * e1 + c[1]) * e0 + c[0];
+        base = halo[hd][hs];
+        stride = g.slab[hd];
+    } else {
+        const int bx = l[0] / g.nb[0], by = l[1] / g.nb[1], bz = l[2] / g.nb[2];
+        const long long blk = bx + (long long)g.bn[0] * (by + (long long)g.bn[1] * bz);
+        idx = blk * g.cpb + ((long long)(l[2] - bz * g.nb[2]) * g.nb[1] + (l[1] - by * g.nb[1])) * g.nb[0] +
+              (l[0] - bx * g.nb[0]);
+        base = u;
+        stride = g.ncell;
+    }
+#pragma unroll
+    for (int v = 0; v < NV; v++) out[v] = base[v * stride + idx];
+#pragma unroll
+    for (int d = 0; d < NV - 2; d++)
+        if (flip[d]) out[1 + d] = -out[1 + d];
+    return true;
+}
+
+// ------------------------------------------------------------ reductions
+__device__ __forceinline__ double warp_min(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = fmin(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+}
+
+// CFL term of one primitive state: min_d dx_d / (|u_d| + c)  (reading R7).
+template <int NV>
+__device__ __forceinline__ double cfl_term(const Geo& g, const double* w) {
+    const double c = sqrt_fast(g.gamma * w[NV - 1] * rcp(w[0]));
+    double best = INFINITY;
+#pragma unroll
+    for (int d = 0; d < NV - 2; d++) best = fmin(best, g.dx[d] * rcp(fabs(w[1 + d]) + c));
+    return best;
+}
+
+// Block-wide min of x -> atomicMin on the u64 bits (positive doubles order
+// like unsigned integers; +inf is the identity).  All threads must call;
+// blockDim.x is a multiple of 32.
+__device__ __forceinline__ void block_min_to(double x, double* red, unsigned long long* acc) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    x = warp_min(x);
+    if (lane == 0) red[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = red[0];
+        for (int w = 1; w < nw; w++) m = fmin(m, red[w]);
+        if (m < INFINITY) atomicMin(acc, (unsigned long long)__double_as_longlong(m));
+    }
+}
+
+}  // namespace dev
+}  // namespace spark

@@ -1,0 +1,424 @@
+// spark_stage.cu — KB1, the fused Spark stage kernel (sm_100a, FP64).
+//
+// One launch = one SSP-RK stage over every block of the rank's sub-box:
+//   guard gather -> EOS cons->prim (block init, Alg. 7) ->
+//   calcLims (reconstruction) -> calcFlux (Riemann) -> updSoln (flux
+//   divergence + RK combination) -> calcEos (positivity / CFL-min epilogue),
+// i.e. the intra-stage chain of Alg. 8 for one stage of
+// lst:spark-nontelescoping, in ONE pass over HBM:
+//   U_out = a U_n + b (U_prev + dt L(U_prev)).
+//
+// Mapping: one CTA per block, one thread per (i,j) column,
+// marching over the block's k planes.  Per plane:
+//   S1 load   plane k+NG of the thread's column into a ring of 2*NG-1 primitive
+//             planes (own column only) and the x/y face halos of plane k into
+//             a padded shared plane `cur` (neighbour block read straight from
+//             the pool, L2-resident; no guard cells are stored in HBM)
+//   S2 recon  cell-centric: each cell's x, y (and z, from the ring) limiter /
+//             smoothness evaluation is done once and gives both edge states
+//   S3 flux   each face once: x/y faces into shared memory, the z face in
+//             registers (carried to the next plane)
+//   S4 update own cell; last stage also the CFL-min epilogue.
+// Block shape is a template parameter for the production shapes (16x16 planes)
+// so that all index arithmetic folds; 0 means "runtime" (any shape <= 256 cells
+// per plane).
+#include <cmath>
+#include <cstdint>
+
+#include "spark_device.cuh"
+#include "spark_internal.h"
+
+namespace spark {
+namespace {
+
+using namespace dev;
+
+constexpr int kThreads = 256;
+
+template <int NV>
+__device__ __forceinline__ void ldg_cons(const double* __restrict__ p, long long stride, double* u) {
+#pragma unroll
+    for (int v = 0; v < NV; v++) u[v] = __ldg(p + v * stride);
+}
+
+template <int NDIM, int RECON, int RS, int NBX, int NBY>
+__global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
+    constexpr int NV = NDIM + 2;
+    constexpr int NG = StencilOf<RECON>::NG;
+    constexpr int R = NG - 1;  // cell-centric reconstruction radius
+    constexpr int RS_ = 2 * NG - 1 > 2 ? 2 * NG - 1 : 2;  // ring slots (planes k-R' .. k+NG alive)
+    constexpr int RING = NDIM == 3 ? RS_ : 0;
+    constexpr int RO = NDIM >= 2 ? NG : 0;  // row offset of the interior in cur
+    const Geo& g = A.g;
+    extern __shared__ double smem[];
+
+    const int nb0 = NBX ? NBX : g.nb[0];
+    const int nb1 = NDIM >= 2 ? (NBY ? NBY : g.nb[1]) : 1;
+    const int nb2 = NDIM >= 3 ? g.nb[2] : 1;
+    const int P = nb0 * nb1;
+    const int tid = threadIdx.x;
+    const bool live = tid < P;
+    const int ti = live ? tid % nb0 : 0, tj = live ? tid / nb0 : 0;
+    const int b = blockIdx.x;
+    const int bx = b % g.bn[0], by = (b / g.bn[0]) % g.bn[1], bz = b / (g.bn[0] * g.bn[1]);
+    const int cx0 = bx * nb0, cy0 = by * nb1, cz0 = bz * nb2;
+    const long long cpb = (long long)nb0 * nb1 * nb2;
+    const long long bbase = (long long)b * cpb;
+    const long long ncell = g.ncell;
+    const double* __restrict__ up = A.uprev;
+
+    const int cw = nb0 + 2 * NG, ch = NDIM >= 2 ? nb1 + 2 * NG : 1;
+    const int CP = cw * ch;
+    const int fxs = nb0 + 1;                   // x faces per row
+    const int fxn = fxs * nb1;
+    const int fyn = NDIM >= 2 ? nb0 * (nb1 + 1) : 0;
+    double* ring = smem;                       // [RING][NV][P]
+    double* cur = ring + RING * NV * P;        // [NV][CP]
+    double* XA = cur + NV * CP;                // [NV][fxn]: L state at x face, then x flux
+    double* XB = XA + NV * fxn;                // [NV][fxn]: R state at x face
+    double* YA = XB + NV * fxn;                // [NV][fyn]
+    double* YB = YA + NV * fyn;                // [NV][fyn]
+
+    const double dt = A.dt_ptr ? *A.dt_ptr : A.dt_value;
+    const double a = A.a, bco = A.b;
+    const double gamma = g.gamma, gm1 = g.gamma - 1.0, gm1i = 1.0 / (g.gamma - 1.0);
+
+    if (A.honor_active && !A.sc->active) {  // t >= t_end: U^(s) = U^(s-1)
+        if (live)
+            for (int kk = 0; kk < nb2; kk++) {
+                const long long idx = bbase + ((long long)kk * nb1 + tj) * nb0 + ti;
+#pragma unroll
+                for (int v = 0; v < NV; v++) A.uout[v * ncell + idx] = up[v * ncell + idx];
+            }
+        return;
+    }
+
+    // Base pointers of the face-neighbour blocks inside this rank's sub-box
+    // (null: boundary or other rank -> general gather).  CTA-uniform.
+    const double* nbp[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+    {
+        const int bc3[3] = {bx, by, bz};
+#pragma unroll
+        for (int d = 0; d < NDIM; d++) {
+            int q[3] = {bx, by, bz};
+            if (bc3[d] > 0) {
+                q[d] = bc3[d] - 1;
+                nbp[d][0] = up + (q[0] + (long long)g.bn[0] * (q[1] + (long long)g.bn[1] * q[2])) * cpb;
+            }
+            q[d] = bc3[d];
+            if (bc3[d] + 1 < g.bn[d]) {
+                q[d] = bc3[d] + 1;
+                nbp[d][1] = up + (q[0] + (long long)g.bn[0] * (q[1] + (long long)g.bn[1] * q[2])) * cpb;
+            }
+        }
+    }
+
+    bool ok = true;
+    // conserved -> primitive of the cell at block-local (x, y, z) (at most one
+    // coordinate outside the block)
+    auto load_prim = [&](int x, int y, int z, double* w) {
+        double u[NV];
+        int d = -1, side = 0, lx = x, ly = y, lz = z;
+        if (x < 0 || x >= nb0) { d = 0; side = x >= nb0; lx = side ? x - nb0 : x + nb0; }
+        else if (NDIM >= 2 && (y < 0 || y >= nb1)) { d = 1; side = y >= nb1; ly = side ? y - nb1 : y + nb1; }
+        else if (NDIM >= 3 && (z < 0 || z >= nb2)) { d = 2; side = z >= nb2; lz = side ? z - nb2 : z + nb2; }
+        const long long off = ((long long)lz * nb1 + ly) * nb0 + lx;
+        // select without dynamic indexing (keeps nbp in registers)
+        const double* nb = d == 0 ? (side ? nbp[0][1] : nbp[0][0])
+                                  : (d == 1 ? (side ? nbp[1][1] : nbp[1][0]) : (side ? nbp[2][1] : nbp[2][0]));
+        if (d < 0) {
+            ldg_cons<NV>(up + bbase + off, ncell, u);
+        } else if (nb) {
+            ldg_cons<NV>(nb + off, ncell, u);
+        } else {
+            fetch_cons<NV>(g, up, A.halo, cx0 + x, cy0 + y, cz0 + z, u);
+        }
+        ok &= cons_to_prim<NV>(u, w, gm1);
+    };
+
+    // z machinery (3-D): ring slot of plane z is (z + NG) mod RS_
+    auto ring_at = [&](int z, int v) -> double& { return ring[(((z + NG) % RS_) * NV + v) * P + tid]; };
+    double zhi[NV];   // L state of the face above the current plane (top edge of cell kk)
+    double fzlo[NV];  // flux through the face below the current plane
+    double fzhi[NV];
+#pragma unroll
+    for (int v = 0; v < NV; v++) zhi[v] = fzlo[v] = fzhi[v] = 0.0;
+
+    // z reconstruction of cell z of this column from the ring
+    auto zrecon = [&](int z, double* lo, double* hi) {
+#pragma unroll
+        for (int v = 0; v < NV; v++) {
+            double s[2 * R + 1];
+#pragma unroll
+            for (int m = 0; m <= 2 * R; m++) s[m] = ring_at(z - R + m, v);
+            recon_cell<RECON>(s, lo[v], hi[v]);
+        }
+    };
+    // flux through the z face between cells z and z+1 of this column
+    auto zflux = [&](int z, double* wl, double* wr, double* f) {
+        if (RECON != 0 && !(positive(wl[0]) && positive(wl[NV - 1]) && positive(wr[0]) && positive(wr[NV - 1]))) {
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                wl[v] = ring_at(z, v);
+                wr[v] = ring_at(z + 1, v);
+            }
+        }
+        riemann<NV, RS, 2>(wl, wr, gamma, gm1i, f);
+    };
+
+    if (NDIM == 3) {
+        if (live) {
+            double w[NV];
+            for (int z = -NG; z < NG - 1; z++) {
+                load_prim(ti, tj, z, w);
+#pragma unroll
+                for (int v = 0; v < NV; v++) ring_at(z, v) = w[v];
+            }
+            double lo[NV], hi[NV], l0[NV];
+            zrecon(-1, l0, hi);  // top edge of cell -1 -> L state of face -1/2
+            load_prim(ti, tj, NG - 1, w);  // replaces plane -NG (dead)
+#pragma unroll
+            for (int v = 0; v < NV; v++) ring_at(NG - 1, v) = w[v];
+            zrecon(0, lo, zhi);  // bottom edge of cell 0 -> R state of face -1/2
+            zflux(-1, hi, lo, fzlo);
+        }
+    }
+
+    const int nhx = 2 * NG * nb1;
+    const int nh = nhx + (NDIM >= 2 ? 2 * NG * nb0 : 0);
+    const int nbr = 2 * nb1 + (NDIM >= 2 ? 2 * nb0 : 0);  // boundary recon items
+    const int nbf = nb1 + (NDIM >= 2 ? nb0 : 0);          // boundary faces (x face 0, y face 0)
+    double cflmin = INFINITY;
+
+    for (int kk = 0; kk < nb2; kk++) {
+        // ---------------------------------------------------------------- S1
+        __syncthreads();
+        if (live) {
+            double w[NV];
+            if (NDIM == 3) {
+                load_prim(ti, tj, kk + NG, w);
+#pragma unroll
+                for (int v = 0; v < NV; v++) ring_at(kk + NG, v) = w[v];
+#pragma unroll
+                for (int v = 0; v < NV; v++) w[v] = ring_at(kk, v);
+            } else {
+                load_prim(ti, tj, kk, w);
+            }
+#pragma unroll
+            for (int v = 0; v < NV; v++) cur[v * CP + (tj + RO) * cw + ti + NG] = w[v];
+        }
+        for (int h = tid; h < nh; h += blockDim.x) {
+            int cx, cy;
+            if (h < nhx) {  // x strips [side][row][depth]
+                const int side = h / (NG * nb1), r = h % (NG * nb1);
+                cy = r / NG;
+                const int dp = r % NG;
+                cx = side ? nb0 + dp : dp - NG;
+            } else {  // y strips [side][depth][col]
+                const int hh = h - nhx;
+                const int side = hh / (NG * nb0), r = hh % (NG * nb0);
+                const int dp = r / nb0;
+                cx = r % nb0;
+                cy = side ? nb1 + dp : dp - NG;
+            }
+            double w[NV];
+            load_prim(cx, cy, kk, w);
+#pragma unroll
+            for (int v = 0; v < NV; v++) cur[v * CP + (cy + RO) * cw + cx + NG] = w[v];
+        }
+        __syncthreads();
+        // ---------------------------------------------------------------- S2
+        double zlo[NV], zhn[NV];
+        if (live) {
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                double s[2 * R + 1], lo, hi;
+                const double* c = cur + v * CP + (tj + RO) * cw + ti + NG;
+#pragma unroll
+                for (int m = 0; m <= 2 * R; m++) s[m] = c[m - R];
+                recon_cell<RECON>(s, lo, hi);
+                XB[v * fxn + tj * fxs + ti] = lo;
+                XA[v * fxn + tj * fxs + ti + 1] = hi;
+                if (NDIM >= 2) {
+#pragma unroll
+                    for (int m = 0; m <= 2 * R; m++) s[m] = c[(m - R) * cw];
+                    recon_cell<RECON>(s, lo, hi);
+                    YB[v * fyn + tj * nb0 + ti] = lo;
+                    YA[v * fyn + (tj + 1) * nb0 + ti] = hi;
+                }
+            }
+            if (NDIM == 3) zrecon(kk + 1, zlo, zhn);
+        }
+        for (int q = tid; q < nbr; q += blockDim.x) {  // edge states from the halo cells
+            const bool xd = q < 2 * nb1;
+            const int qq = xd ? q : q - 2 * nb1;
+            const int side = xd ? qq / nb1 : qq / nb0;
+            const int r = xd ? qq % nb1 : qq % nb0;
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                double s[2 * R + 1], lo, hi;
+                if (xd) {
+                    const double* c = cur + v * CP + (r + RO) * cw + (side ? nb0 : -1) + NG;
+#pragma unroll
+                    for (int m = 0; m <= 2 * R; m++) s[m] = c[m - R];
+                } else {
+                    const double* c = cur + v * CP + ((side ? nb1 : -1) + RO) * cw + r + NG;
+#pragma unroll
+                    for (int m = 0; m <= 2 * R; m++) s[m] = c[(m - R) * cw];
+                }
+                recon_cell<RECON>(s, lo, hi);
+                if (xd) {
+                    if (side) XB[v * fxn + r * fxs + nb0] = lo;
+                    else XA[v * fxn + r * fxs] = hi;
+                } else {
+                    if (side) YB[v * fyn + nb1 * nb0 + r] = lo;
+                    else YA[v * fyn + r] = hi;
+                }
+            }
+        }
+        __syncthreads();
+        // ---------------------------------------------------------------- S3
+        // x face at column f of row r: cells (f-1, f); y face at row f of column r
+        auto xface = [&](int r, int f) {
+            double wl[NV], wr[NV], fl[NV];
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                wl[v] = XA[v * fxn + r * fxs + f];
+                wr[v] = XB[v * fxn + r * fxs + f];
+            }
+            if (RECON != 0 && !(positive(wl[0]) && positive(wl[NV - 1]) && positive(wr[0]) && positive(wr[NV - 1]))) {
+#pragma unroll
+                for (int v = 0; v < NV; v++) {
+                    wl[v] = cur[v * CP + (r + RO) * cw + f - 1 + NG];
+                    wr[v] = cur[v * CP + (r + RO) * cw + f + NG];
+                }
+            }
+            riemann<NV, RS, 0>(wl, wr, gamma, gm1i, fl);
+#pragma unroll
+            for (int v = 0; v < NV; v++) XA[v * fxn + r * fxs + f] = fl[v];
+        };
+        auto yface = [&](int r, int f) {
+            double wl[NV], wr[NV], fl[NV];
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                wl[v] = YA[v * fyn + f * nb0 + r];
+                wr[v] = YB[v * fyn + f * nb0 + r];
+            }
+            if (RECON != 0 && !(positive(wl[0]) && positive(wl[NV - 1]) && positive(wr[0]) && positive(wr[NV - 1]))) {
+#pragma unroll
+                for (int v = 0; v < NV; v++) {
+                    wl[v] = cur[v * CP + (f - 1 + NG) * cw + r + NG];
+                    wr[v] = cur[v * CP + (f + NG) * cw + r + NG];
+                }
+            }
+            riemann<NV, RS, 1>(wl, wr, gamma, gm1i, fl);
+#pragma unroll
+            for (int v = 0; v < NV; v++) YA[v * fyn + f * nb0 + r] = fl[v];
+        };
+        if (live) {
+            xface(tj, ti + 1);
+            if (NDIM >= 2) yface(ti, tj + 1);
+            if (NDIM == 3) {
+                zflux(kk, zhi, zlo, fzhi);
+#pragma unroll
+                for (int v = 0; v < NV; v++) zhi[v] = zhn[v];
+            }
+        }
+        for (int q = tid; q < nbf; q += blockDim.x) {
+            if (q < nb1) xface(q, 0);
+            else yface(q - nb1, 0);
+        }
+        __syncthreads();
+        // ---------------------------------------------------------------- S4
+        if (live) {
+            const long long idx = bbase + ((long long)kk * nb1 + tj) * nb0 + ti;
+            double un[NV];
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                const double dfx = (XA[v * fxn + tj * fxs + ti + 1] - XA[v * fxn + tj * fxs + ti]) * g.rdx[0];
+                double L;
+                if (NDIM == 1) {
+                    L = -dfx;
+                } else {
+                    const double dfy = (YA[v * fyn + (tj + 1) * nb0 + ti] - YA[v * fyn + tj * nb0 + ti]) * g.rdx[1];
+                    if (NDIM == 2) L = -(dfx + dfy);
+                    else L = -(dfx + dfy) - (fzhi[v] - fzlo[v]) * g.rdx[2];
+                }
+                const double u0 = up[v * ncell + idx];
+                const double uo = fma(bco, fma(dt, L, u0), a != 0.0 ? a * A.un[v * ncell + idx] : 0.0);
+                A.uout[v * ncell + idx] = uo;
+                un[v] = uo;
+                fzlo[v] = fzhi[v];
+            }
+            if (A.last) {
+                double w[NV];
+                ok &= cons_to_prim<NV>(un, w, gm1);
+                cflmin = fmin(cflmin, cfl_term<NV>(g, w));
+            }
+        }
+    }
+    if (!ok) atomicOr(&A.sc->status, 1);
+    if (A.last) {
+        __syncthreads();
+        block_min_to(cflmin, cur, &A.sc->acc);  // cur is dead here
+    }
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int NDIM, int RECON, int RS, int NBX, int NBY>
+cudaError_t launch_t(const StageArgs& a, cudaStream_t s) {
+    const size_t smem = stage_smem_bytes(a.g, RECON);
+    auto k = stage_kernel<NDIM, RECON, RS, NBX, NBY>;
+    cudaError_t e = set_smem(k, smem);
+    if (e != cudaSuccess) return e;
+    const long long nblk = (long long)a.g.bn[0] * a.g.bn[1] * a.g.bn[2];
+    k<<<(unsigned)nblk, stage_block_threads(a.g), smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+// Production shapes (16x16 planes) get compile-time block extents.
+template <int NDIM, int RECON, int RS>
+cudaError_t launch_shape(const StageArgs& a, cudaStream_t s) {
+    if (NDIM >= 2 && a.g.nb[0] == 16 && a.g.nb[1] == 16) return launch_t<NDIM, RECON, RS, 16, 16>(a, s);
+    return launch_t<NDIM, RECON, RS, 0, 0>(a, s);
+}
+
+template <int NDIM>
+cudaError_t launch_d(const StageArgs& a, int recon, int riemann, cudaStream_t s) {
+    if (recon == 0) return riemann ? launch_shape<NDIM, 0, 1>(a, s) : launch_shape<NDIM, 0, 0>(a, s);
+    if (recon == 1) return riemann ? launch_shape<NDIM, 1, 1>(a, s) : launch_shape<NDIM, 1, 0>(a, s);
+    return riemann ? launch_shape<NDIM, 2, 1>(a, s) : launch_shape<NDIM, 2, 0>(a, s);
+}
+
+}  // namespace
+
+int stage_block_threads(const Geo& g) {
+    const int P = g.nb[0] * (g.ndim >= 2 ? g.nb[1] : 1);
+    return ((P + 31) / 32) * 32;
+}
+
+size_t stage_smem_bytes(const Geo& g, int recon) {
+    const int NG = recon == 2 ? 3 : (recon == 1 ? 2 : 1);
+    const int NV = g.ndim + 2;
+    const int nb0 = g.nb[0], nb1 = g.ndim >= 2 ? g.nb[1] : 1;
+    const size_t P = (size_t)nb0 * nb1;
+    const size_t slots = 2 * NG - 1 > 2 ? 2 * NG - 1 : 2;
+    const size_t ring = g.ndim == 3 ? slots * NV * P : 0;
+    const size_t cw = nb0 + 2 * NG, ch = g.ndim >= 2 ? nb1 + 2 * NG : 1;
+    const size_t cur = NV * cw * ch;
+    const size_t fx = 2 * NV * (size_t)(nb0 + 1) * nb1;
+    const size_t fy = g.ndim >= 2 ? 2 * NV * (size_t)nb0 * (nb1 + 1) : 0;
+    return (ring + cur + fx + fy) * sizeof(double);
+}
+
+cudaError_t launch_stage(const StageArgs& a, int recon, int riemann, cudaStream_t s) {
+    if (a.g.ndim == 1) return launch_d<1>(a, recon, riemann, s);
+    if (a.g.ndim == 2) return launch_d<2>(a, recon, riemann, s);
+    return launch_d<3>(a, recon, riemann, s);
+}
+
+}  // namespace spark

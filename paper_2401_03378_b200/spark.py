@@ -25,6 +25,7 @@ EXPORTS = [
     "spark_finalize", "spark_last_error", "spark_set_state", "spark_set_primitive", "spark_get_state",
     "spark_get_time", "spark_get_cfl_min", "spark_fill_guardcells", "spark_step", "spark_advance",
     "spark_step_group", "spark_stage_apply", "spark_profile_enable", "spark_profile_read",
+    "spark_selftest_riemann",
 ]
 
 
@@ -118,6 +119,7 @@ def lib() -> ctypes.CDLL:
         "spark_stage_apply": (i32, [vp, vp, vp, d, d, d, vp]),
         "spark_profile_enable": (i32, [vp, i32]),
         "spark_profile_read": (i32, [vp, P(d), P(i64), P(i64)]),
+        "spark_selftest_riemann": (i32, [i32, i32, i32, i32, d, i64, P(d), P(d), P(d)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -176,6 +178,18 @@ def nccl_unique_id() -> bytes:
     buf = (ctypes.c_uint8 * 128)()
     _check(lib().spark_nccl_unique_id(buf), what="nccl_unique_id")
     return bytes(buf)
+
+
+def selftest_riemann(kind: int, ndim: int, direction: int, gamma: float, wl: np.ndarray, wr: np.ndarray,
+                     device: int = 0) -> np.ndarray:
+    """Device Riemann fluxes for face states wl, wr ([n][ndim+2], unrotated primitive)."""
+    wl = np.ascontiguousarray(wl, dtype=np.float64)
+    wr = np.ascontiguousarray(wr, dtype=np.float64)
+    f = np.empty_like(wl)
+    dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    _check(lib().spark_selftest_riemann(device, kind, ndim, direction, gamma, wl.shape[0], dp(wl), dp(wr), dp(f)),
+           what="selftest_riemann")
+    return f
 
 
 def local_shape(cfg: dict, rank: int = 0, nranks: int = 1):

@@ -70,6 +70,27 @@ STAGE_CASES = [
 ]
 
 
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("ndim", [1, 2, 3])
+def test_device_riemann(sp, kind, ndim):
+    """The device Riemann solver (calcFlux of KB1) vs the oracle, face by face,
+    sub- and supersonic states, every normal direction (regression for an nvcc
+    miscompile of the HLLC K-side selects)."""
+    g = np.random.Generator(np.random.PCG64(40 + ndim + 10 * kind))
+    nv, n = ndim + 2, 4000
+    W = np.empty((2, n, nv))
+    W[:, :, 0] = g.uniform(0.05, 5.0, (2, n))
+    W[:, :, 1:nv - 1] = g.uniform(-1, 1, (2, n, nv - 2)) * np.where(np.arange(n) % 4 == 0, 4.0, 1.0)[None, :, None]
+    W[:, :, nv - 1] = g.uniform(0.01, 5.0, (2, n))
+    for d in range(ndim):
+        f = sp.selftest_riemann(kind, ndim, d, 1.4, W[0], W[1])
+        order = [0, 1 + d] + [1 + e for e in range(ndim) if e != d] + [nv - 1]
+        for q in range(0, n, 7):
+            fo = np.empty(nv)
+            fo[order] = oracle.riemann(kind, 1.4, W[0, q, order], W[1, q, order])
+            assert np.allclose(f[q], fo, rtol=1e-12, atol=1e-13 * (np.abs(fo).max() + 1)), (q, d, f[q], fo)
+
+
 @pytest.mark.parametrize("p", STAGE_CASES, ids=lambda p: p.name)
 def test_prim_to_cons(sp, p):
     W = si.random_state(p, 3)
@@ -283,6 +304,16 @@ def test_nonphysical_rollback(sp):
     s.set_state(U2)
     with pytest.raises(sp.NonPhysicalError):
         s.step(dt=1e-4, sync=True)
+    # rolled back: U^n of the failed step is the current state, time unchanged
+    assert np.array_equal(state(s), U2)
+    t, n, _ = s.time()
+    assert t == 0.0 and n == 0
+    # a physical state steps normally afterwards
+    s.set_state(U)
+    s.step(dt=1e-4, sync=True)
+    # without a sync point the error surfaces at the next synchronising call
+    s.set_state(U2)
+    s.step(dt=1e-4)
     with pytest.raises(sp.NonPhysicalError):
         state(s)
 
