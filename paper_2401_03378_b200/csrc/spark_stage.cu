@@ -93,46 +93,32 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
         return;
     }
 
-    // Base pointers of the face-neighbour blocks inside this rank's sub-box
-    // (null: boundary or other rank -> general gather).  CTA-uniform.
-    const double* nbp[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
-    {
-        const int bc3[3] = {bx, by, bz};
-#pragma unroll
-        for (int d = 0; d < NDIM; d++) {
-            int q[3] = {bx, by, bz};
-            if (bc3[d] > 0) {
-                q[d] = bc3[d] - 1;
-                nbp[d][0] = up + (q[0] + (long long)g.bn[0] * (q[1] + (long long)g.bn[1] * q[2])) * cpb;
-            }
-            q[d] = bc3[d];
-            if (bc3[d] + 1 < g.bn[d]) {
-                q[d] = bc3[d] + 1;
-                nbp[d][1] = up + (q[0] + (long long)g.bn[0] * (q[1] + (long long)g.bn[1] * q[2])) * cpb;
-            }
-        }
-    }
-
     bool ok = true;
     // conserved -> primitive of the cell at block-local (x, y, z) (at most one
     // coordinate outside the block)
-    auto load_prim = [&](int x, int y, int z, double* w) {
-        double u[NV];
+    auto load_cons = [&](int x, int y, int z, double* u) {
         int d = -1, side = 0, lx = x, ly = y, lz = z;
         if (x < 0 || x >= nb0) { d = 0; side = x >= nb0; lx = side ? x - nb0 : x + nb0; }
         else if (NDIM >= 2 && (y < 0 || y >= nb1)) { d = 1; side = y >= nb1; ly = side ? y - nb1 : y + nb1; }
         else if (NDIM >= 3 && (z < 0 || z >= nb2)) { d = 2; side = z >= nb2; lz = side ? z - nb2 : z + nb2; }
         const long long off = ((long long)lz * nb1 + ly) * nb0 + lx;
-        // select without dynamic indexing (keeps nbp in registers)
-        const double* nb = d == 0 ? (side ? nbp[0][1] : nbp[0][0])
-                                  : (d == 1 ? (side ? nbp[1][1] : nbp[1][0]) : (side ? nbp[2][1] : nbp[2][0]));
+        // face-neighbour block inside this rank's sub-box (else: general gather)
+        int q0 = bx, q1 = by, q2 = bz;
+        bool inside = true;
+        if (d == 0) { q0 += side ? 1 : -1; inside = q0 >= 0 && q0 < g.bn[0]; }
+        if (d == 1) { q1 += side ? 1 : -1; inside = q1 >= 0 && q1 < g.bn[1]; }
+        if (d == 2) { q2 += side ? 1 : -1; inside = q2 >= 0 && q2 < g.bn[2]; }
         if (d < 0) {
             ldg_cons<NV>(up + bbase + off, ncell, u);
-        } else if (nb) {
-            ldg_cons<NV>(nb + off, ncell, u);
+        } else if (inside) {
+            ldg_cons<NV>(up + (q0 + (long long)g.bn[0] * (q1 + (long long)g.bn[1] * q2)) * cpb + off, ncell, u);
         } else {
             fetch_cons<NV>(g, up, A.halo, cx0 + x, cy0 + y, cz0 + z, u);
         }
+    };
+    auto load_prim = [&](int x, int y, int z, double* w) {
+        double u[NV];
+        load_cons(x, y, z, u);
         ok &= cons_to_prim<NV>(u, w, gm1);
     };
 
@@ -190,13 +176,18 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
     const int nbf = nb1 + (NDIM >= 2 ? nb0 : 0);          // boundary faces (x face 0, y face 0)
     double cflmin = INFINITY;
 
+    // raw conserved values of this column's plane kk+NG, loaded one plane ahead
+    double pre[NV];
+    if (NDIM == 3 && live) load_cons(ti, tj, NG, pre);
+
     for (int kk = 0; kk < nb2; kk++) {
         // ---------------------------------------------------------------- S1
         __syncthreads();
         if (live) {
             double w[NV];
             if (NDIM == 3) {
-                load_prim(ti, tj, kk + NG, w);
+                ok &= cons_to_prim<NV>(pre, w, gm1);
+                if (kk + 1 < nb2) load_cons(ti, tj, kk + 1 + NG, pre);  // prefetch the next plane
 #pragma unroll
                 for (int v = 0; v < NV; v++) ring_at(kk + NG, v) = w[v];
 #pragma unroll
@@ -229,6 +220,16 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
         __syncthreads();
         // ---------------------------------------------------------------- S2
         double zlo[NV], zhn[NV];
+        // operands of the S4 update, requested now so the loads overlap S2/S3
+        double u0v[NV], unv[NV];
+        const long long cidx = bbase + ((long long)kk * nb1 + tj) * nb0 + ti;
+        if (live) {
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                u0v[v] = __ldg(up + v * ncell + cidx);
+                unv[v] = a != 0.0 ? __ldg(A.un + v * ncell + cidx) : 0.0;
+            }
+        }
         if (live) {
 #pragma unroll
             for (int v = 0; v < NV; v++) {
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
         __syncthreads();
         // ---------------------------------------------------------------- S4
         if (live) {
-            const long long idx = bbase + ((long long)kk * nb1 + tj) * nb0 + ti;
+            const long long idx = cidx;
             double un[NV];
 #pragma unroll
             for (int v = 0; v < NV; v++) {
@@ -344,8 +345,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
                     if (NDIM == 2) L = -(dfx + dfy);
                     else L = -(dfx + dfy) - (fzhi[v] - fzlo[v]) * g.rdx[2];
                 }
-                const double u0 = up[v * ncell + idx];
-                const double uo = fma(bco, fma(dt, L, u0), a != 0.0 ? a * A.un[v * ncell + idx] : 0.0);
+                const double uo = fma(bco, fma(dt, L, u0v[v]), a * unv[v]);
                 A.uout[v * ncell + idx] = uo;
                 un[v] = uo;
                 fzlo[v] = fzhi[v];
