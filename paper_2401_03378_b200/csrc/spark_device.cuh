@@ -72,12 +72,17 @@ __host__ __device__ __forceinline__ bool positive(double x) { return dbits(x) > 
 // one of smaller magnitude (ties: b).  Integer pipe only; bitwise equal to
 // the oracle's comparison form (reading R2).
 __host__ __device__ __forceinline__ double minmod(double a, double b) {
+    // m = min(|a|, |b|) carries the sign of a (= sign of b when kept); a zero
+    // m gives a signed zero, which W +- d/2 turns into W exactly, as +0 does.
+    const double m = fmin(fabs(a), fabs(b));
+#ifdef __CUDA_ARCH__
+    const int ha = __double2hiint(a), hb = __double2hiint(b);
+    const double r = __hiloint2double(__double2hiint(m) | (ha & 0x80000000), __double2loint(m));
+    return (ha ^ hb) >= 0 ? r : 0.0;
+#else
     const long long ia = dbits(a), ib = dbits(b);
-    const unsigned long long ma = (unsigned long long)ia & 0x7fffffffffffffffull;
-    const unsigned long long mb = (unsigned long long)ib & 0x7fffffffffffffffull;
-    const bool keep = ((ia ^ ib) >= 0) && ma != 0 && mb != 0;
-    const double r = ma < mb ? a : b;
-    return keep ? r : 0.0;
+    return (ia ^ ib) >= 0 ? copysign(m, a) : 0.0;
+#endif
 }
 
 // ------------------------------------------------------------------- EOS

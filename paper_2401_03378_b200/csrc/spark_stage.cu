@@ -250,31 +250,31 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
             }
             if (NDIM == 3) zrecon(kk + 1, zlo, zhn);
         }
-        for (int q = tid; q < nbr; q += blockDim.x) {  // edge states from the halo cells
+        // edge states from the halo cells: one (cell, variable) item per thread
+        // round so the extra work spreads over all warps
+        for (int qv = tid; qv < nbr * NV; qv += blockDim.x) {
+            const int v = qv / nbr, q = qv - v * nbr;
             const bool xd = q < 2 * nb1;
             const int qq = xd ? q : q - 2 * nb1;
             const int side = xd ? qq / nb1 : qq / nb0;
             const int r = xd ? qq % nb1 : qq % nb0;
+            double s[2 * R + 1], lo, hi;
+            if (xd) {
+                const double* c = cur + v * CP + (r + RO) * cw + (side ? nb0 : -1) + NG;
 #pragma unroll
-            for (int v = 0; v < NV; v++) {
-                double s[2 * R + 1], lo, hi;
-                if (xd) {
-                    const double* c = cur + v * CP + (r + RO) * cw + (side ? nb0 : -1) + NG;
+                for (int m = 0; m <= 2 * R; m++) s[m] = c[m - R];
+            } else {
+                const double* c = cur + v * CP + ((side ? nb1 : -1) + RO) * cw + r + NG;
 #pragma unroll
-                    for (int m = 0; m <= 2 * R; m++) s[m] = c[m - R];
-                } else {
-                    const double* c = cur + v * CP + ((side ? nb1 : -1) + RO) * cw + r + NG;
-#pragma unroll
-                    for (int m = 0; m <= 2 * R; m++) s[m] = c[(m - R) * cw];
-                }
-                recon_cell<RECON>(s, lo, hi);
-                if (xd) {
-                    if (side) XB[v * fxn + r * fxs + nb0] = lo;
-                    else XA[v * fxn + r * fxs] = hi;
-                } else {
-                    if (side) YB[v * fyn + nb1 * nb0 + r] = lo;
-                    else YA[v * fyn + r] = hi;
-                }
+                for (int m = 0; m <= 2 * R; m++) s[m] = c[(m - R) * cw];
+            }
+            recon_cell<RECON>(s, lo, hi);
+            if (xd) {
+                if (side) XB[v * fxn + r * fxs + nb0] = lo;
+                else XA[v * fxn + r * fxs] = hi;
+            } else {
+                if (side) YB[v * fyn + nb1 * nb0 + r] = lo;
+                else YA[v * fyn + r] = hi;
             }
         }
         __syncthreads();
