@@ -182,7 +182,9 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
 
     for (int kk = 0; kk < nb2; kk++) {
         // ---------------------------------------------------------------- S1
-        __syncthreads();
+        // No barrier before S1: cur was last read in S3 of the previous plane
+        // (fenced by the S3->S4 barrier) and the face arrays written in S2 are
+        // fenced by the S1->S2 barrier; the ring is per-thread.
         if (live) {
             double w[NV];
             if (NDIM == 3) {
