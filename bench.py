@@ -64,13 +64,27 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
-def ncu_traffic(name: str):
-    """dram bytes per stage-kernel launch from the committed ncu summary (or None)."""
+def ncu_field(name: str, key: str):
+    """A per-config field of the committed ncu summary (profiles/ncu_summary.json) or None."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(name, {}).get("dram_bytes_per_launch")
+        return d.get(name, {}).get(key)
+    except Exception:
+        return None
+
+
+def ncu_traffic(name: str):
+    """dram bytes per stage-kernel launch from the committed ncu summary (or None)."""
+    return ncu_field(name, "dram_bytes_per_launch")
+
+
+def fp64_peak_rate():
+    """Measured B200 DFMA issue rate (instr/s) from profiles/fp64_peak.json."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            return float(json.load(f)["dfma_per_s"])
     except Exception:
         return None
 
@@ -290,6 +304,18 @@ def main():
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                 "kernel": "stage_kernel (KB1)", "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
                 "stage_kernel_share": (stage_ms / ms) if ms > 0 else None}
+    # FP64 view (the binding unit): executed FP64 instructions
+    # per zone-update (ncu, profiles/ncu_summary.json) x the kernel's zone rate,
+    # against the measured DFMA issue rate (tools/fp64_peak.cu, profiles/fp64_peak.json)
+    roofline_fp64 = None
+    fp64_per_zone = ncu_field(p.name, "fp64_inst_per_zone")
+    fp64_peak = fp64_peak_rate()
+    if fp64_per_zone and fp64_peak:
+        zu_rate_kernel = cells_local * p.rk_stages * args.steps / (stage_ms * 1e-3)
+        ach = fp64_per_zone * zu_rate_kernel
+        roofline_fp64 = {"bound": "alu", "achieved": ach / 1e12, "peak": fp64_peak / 1e12,
+                         "unit": "T FP64 instr/s", "frac": ach / fp64_peak,
+                         "per_zone": fp64_per_zone, "source": "ncu instruction counts x live kernel time"}
 
     # ---- end to end through the public API with host buffers
     e2e = None
@@ -329,7 +355,8 @@ def main():
                        "block": list(p.nb), "blocks": list(p.nblk), "recon": ["first", "plm", "weno5"][p.recon],
                        "riemann": ["hll", "hllc"][p.riemann], "rk_stages": p.rk_stages, "ng": p.ng,
                        "parallelism": f"blocks over {world} GPU(s)", "l2": "state per copy > L2 (no flush needed)"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": total_launches,
+            "roofline": roofline, "roofline_fp64": roofline_fp64, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": total_launches,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
