@@ -55,6 +55,19 @@ __host__ __device__ __forceinline__ double sqrt_fast(double a) {
     return fma(h * r, fma(0.375, r, 0.5), h);
 }
 
+// 1/sqrt(a), a > 0: y (1 + r/2 + 3r^2/8), r = 1 - a y^2.
+__host__ __device__ __forceinline__ double rsqrt_fast(double a) {
+#ifdef __CUDA_ARCH__
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    y = __hiloint2double(__double2hiint(y), 0);
+#else
+    double y = (double)(1.0f / sqrtf((float)a));
+#endif
+    const double r = fma(-a * y, y, 1.0);
+    return fma(y * r, fma(0.375, r, 0.5), y);
+}
+
 // x > 0 for non-NaN x, on the integer pipe (+0 and -0 are not positive).
 __host__ __device__ __forceinline__ long long dbits(double x) {
 #ifdef __CUDA_ARCH__
@@ -116,31 +129,34 @@ __host__ __device__ __forceinline__ void recon_cell(const double* s, double& lo,
         lo = fma(-0.5, d, s[1]);
         hi = fma(0.5, d, s[1]);
     } else {  // WENO5-JS, both edges from shared smoothness indicators
+        // Same weights as the textbook form, regrouped for fewer FP64 operations:
+        //   beta'_k = 4 beta_k = (13/3) t_k^2 + u_k^2,  (eps + beta)^2 = (4 eps + beta')^2 / 16
+        //   (the common 1/16 cancels in the normalised weights);
+        //   alpha_k ~ d_k / s_k is multiplied through by s0 s1 s2 (one reciprocal
+        //   per edge) and by 10 (linear weights 1, 6, 3); the candidates' 1/6 moves
+        //   into the denominator.
         const double a = s[0], b = s[1], c = s[2], d = s[3], e = s[4];
-        const double eps = 1e-6;
-        const double t0 = a - 2.0 * b + c, u0 = a - 4.0 * b + 3.0 * c;
-        const double t1 = b - 2.0 * c + d, u1 = b - d;
-        const double t2 = c - 2.0 * d + e, u2 = 3.0 * c - 4.0 * d + e;
-        const double b0 = fma(13.0 / 12.0 * t0, t0, 0.25 * u0 * u0);
-        const double b1 = fma(13.0 / 12.0 * t1, t1, 0.25 * u1 * u1);
-        const double b2 = fma(13.0 / 12.0 * t2, t2, 0.25 * u2 * u2);
-        const double e0 = eps + b0, e1 = eps + b1, e2 = eps + b2;
+        constexpr double eps4 = 4e-6, k13 = 13.0 / 3.0;
+        const double t0 = fma(-2.0, b, a) + c, u0 = fma(3.0, c, fma(-4.0, b, a));
+        const double t1 = fma(-2.0, c, b) + d, u1 = b - d;
+        const double t2 = fma(-2.0, d, c) + e, u2 = fma(3.0, c, fma(-4.0, d, e));
+        const double e0 = eps4 + fma(k13 * t0, t0, u0 * u0);
+        const double e1 = eps4 + fma(k13 * t1, t1, u1 * u1);
+        const double e2 = eps4 + fma(k13 * t2, t2, u2 * u2);
         const double s0 = e0 * e0, s1 = e1 * e1, s2 = e2 * e2;
-        // alpha_k = d_k / s_k ; multiply through by s0 s1 s2 (one reciprocal per edge)
-        const double P0 = s1 * s2, P1 = s0 * s2, P2 = s0 * s1;
-        constexpr double k6 = 1.0 / 6.0;
-        // right edge (i+1/2): linear weights (0.1, 0.6, 0.3) on stencils (a,b,c), (b,c,d), (c,d,e)
-        const double q0 = (2.0 * a - 7.0 * b + 11.0 * c) * k6;
-        const double q1 = (-b + 5.0 * c + 2.0 * d) * k6;
-        const double q2 = (2.0 * c + 5.0 * d - e) * k6;
-        const double w0 = 0.1 * P0, w1 = 0.6 * P1, w2 = 0.3 * P2;
-        hi = fma(w0, q0, fma(w1, q1, w2 * q2)) * rcp(w0 + w1 + w2);
-        // left edge (i-1/2): the mirrored stencil, weights (0.1, 0.6, 0.3) on (e,d,c), (d,c,b), (c,b,a)
-        const double r0 = (2.0 * e - 7.0 * d + 11.0 * c) * k6;
-        const double r1 = (-d + 5.0 * c + 2.0 * b) * k6;
-        const double r2 = (2.0 * c + 5.0 * b - a) * k6;
-        const double v0 = 0.1 * P2, v1 = 0.6 * P1, v2 = 0.3 * P0;
-        lo = fma(v0, r0, fma(v1, r1, v2 * r2)) * rcp(v0 + v1 + v2);
+        const double P0 = s1 * s2, P1 = 6.0 * (s0 * s2), P2 = s0 * s1;
+        // right edge (i+1/2): stencils (a,b,c), (b,c,d), (c,d,e), weights 1 : 6 : 3
+        const double Q0 = fma(11.0, c, fma(-7.0, b, 2.0 * a));
+        const double Q1 = fma(2.0, d, fma(5.0, c, -b));
+        const double Q2 = fma(5.0, d, fma(2.0, c, -e));
+        const double w2 = 3.0 * P2;
+        hi = fma(P0, Q0, fma(P1, Q1, w2 * Q2)) * rcp(6.0 * (P0 + P1 + w2));
+        // left edge (i-1/2): the mirrored stencils (e,d,c), (d,c,b), (c,b,a), weights 1 : 6 : 3
+        const double R0 = fma(11.0, c, fma(-7.0, d, 2.0 * e));
+        const double R1 = fma(2.0, b, fma(5.0, c, -d));
+        const double R2 = fma(5.0, b, fma(2.0, c, -a));
+        const double v2 = 3.0 * P0;
+        lo = fma(P2, R0, fma(P1, R1, v2 * R2)) * rcp(6.0 * (P2 + P1 + v2));
     }
 }
 
@@ -154,8 +170,9 @@ __host__ __device__ __forceinline__ void riemann(const double* wl, const double*
     constexpr int N = 1 + D;
     const double rl = wl[0], ul = wl[N], pl = wl[NV - 1];
     const double rr = wr[0], ur = wr[N], pr = wr[NV - 1];
-    const double irl = rcp(rl), irr = rcp(rr);
-    const double cl = sqrt_fast(gamma * pl * irl), cr = sqrt_fast(gamma * pr * irr);
+    // c = sqrt(gamma p / rho) = gamma p / sqrt(gamma p rho): no reciprocal of rho needed
+    const double gpl = gamma * pl, gpr = gamma * pr;
+    const double cl = gpl * rsqrt_fast(gpl * rl), cr = gpr * rsqrt_fast(gpr * rr);
     const double sl = fmin(ul - cl, ur - cr);
     const double sr = fmax(ul + cl, ur + cr);
     if (RS == 1) {
@@ -167,8 +184,9 @@ __host__ __device__ __forceinline__ void riemann(const double* wl, const double*
         double w[NV];
 #pragma unroll
         for (int v = 0; v < NV; v++) w[v] = left ? wl[v] : wr[v];
-        const double sk = left ? sl : sr, qk = left ? ql : qr, irho = left ? irl : irr;
+        const double sk = left ? sl : sr, qk = left ? ql : qr;
         const double rho = w[0], un = w[N], p = w[NV - 1];
+        const double irho = rcp(rho);
         double u2 = 0.0;
 #pragma unroll
         for (int d = 1; d < NV - 1; d++) u2 = fma(w[d], w[d], u2);
