@@ -72,6 +72,6 @@ cudaError_t launch_group_min(const AccPtrs& p, int n, cudaStream_t s);
 cudaError_t launch_selftest_riemann(int riemann, int ndim, int dir, double gamma, int64_t n, const double* wl,
                                     const double* wr, double* f);
 size_t stage_smem_bytes(const Geo& g, int recon);
-int stage_block_threads(const Geo& g);
+int stage_block_threads(const Geo& g, int recon);
 
 }  // namespace spark

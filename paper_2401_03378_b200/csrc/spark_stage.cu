@@ -35,14 +35,39 @@ using namespace dev;
 
 constexpr int kThreads = 256;
 
+// Launch policy of a specialisation (host and device agree through this).
+//   stage_ops:      the S4 operands U^(s-1), U^n of the plane are copied to
+//                   shared memory with cp.async (no registers held across S2/S3)
+//   boundary_warp:  a 9th warp does all boundary work (halo loads, halo-cell
+//                   reconstruction, block-boundary faces) so the 8 column warps'
+//                   phases are balanced; needs <= 112 registers (2 CTAs/SM)
+__host__ __device__ constexpr bool policy_stage_ops(int ndim, int recon, int nbx, int nby) {
+    return nbx == 16 && nby == 16 && ndim == 3 && recon <= 1;
+}
+__host__ __device__ constexpr bool policy_boundary_warp(int ndim, int recon, int nbx, int nby) {
+    return nbx == 16 && nby == 16 && ndim == 2 && recon >= 0;
+}
+__host__ __device__ constexpr int policy_block(int ndim, int recon, int nbx, int nby) {
+    return policy_boundary_warp(ndim, recon, nbx, nby) ? kThreads + 32 : kThreads;
+}
+
 template <int NV>
 __device__ __forceinline__ void ldg_cons(const double* __restrict__ p, long long stride, double* u) {
 #pragma unroll
     for (int v = 0; v < NV; v++) u[v] = __ldg(p + v * stride);
 }
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 template <int NDIM, int RECON, int RS, int NBX, int NBY>
-__global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
+__global__ void __launch_bounds__(policy_block(NDIM, RECON, NBX, NBY), 2) stage_kernel(const StageArgs A) {
+    constexpr bool STAGE_OPS = policy_stage_ops(NDIM, RECON, NBX, NBY);
+    constexpr bool BW = policy_boundary_warp(NDIM, RECON, NBX, NBY);
     constexpr int NV = NDIM + 2;
     constexpr int NG = StencilOf<RECON>::NG;
     constexpr int R = NG - 1;  // cell-centric reconstruction radius
@@ -78,6 +103,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
     double* XB = XA + NV * fxn;                // [NV][fxn]: R state at x face
     double* YA = XB + NV * fxn;                // [NV][fyn]
     double* YB = YA + NV * fyn;                // [NV][fyn]
+    double* stg = YB + NV * fyn;               // [2][NV][P] staged S4 operands (STAGE_OPS)
 
     const double dt = A.dt_ptr ? *A.dt_ptr : A.dt_value;
     const double a = A.a, bco = A.b;
@@ -170,6 +196,9 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
         }
     }
 
+    // boundary work items: the boundary warp (tid >= 256) or all threads
+    const int wbeg = BW ? kThreads : 0;
+    const int wstep = BW ? 32 : (int)blockDim.x;
     const int nhx = 2 * NG * nb1;
     const int nh = nhx + (NDIM >= 2 ? 2 * NG * nb0 : 0);
     const int nbr = 2 * nb1 + (NDIM >= 2 ? 2 * nb0 : 0);  // boundary recon items
@@ -200,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
 #pragma unroll
             for (int v = 0; v < NV; v++) cur[v * CP + (tj + RO) * cw + ti + NG] = w[v];
         }
-        for (int h = tid; h < nh; h += blockDim.x) {
+        for (int h = tid - wbeg; h >= 0 && h < nh; h += wstep) {
             int cx, cy;
             if (h < nhx) {  // x strips [side][row][depth]
                 const int side = h / (NG * nb1), r = h % (NG * nb1);
@@ -226,10 +255,19 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
         double u0v[NV], unv[NV];
         const long long cidx = bbase + ((long long)kk * nb1 + tj) * nb0 + ti;
         if (live) {
+            if (STAGE_OPS) {
 #pragma unroll
-            for (int v = 0; v < NV; v++) {
-                u0v[v] = __ldg(up + v * ncell + cidx);
-                unv[v] = a != 0.0 ? __ldg(A.un + v * ncell + cidx) : 0.0;
+                for (int v = 0; v < NV; v++) {
+                    cp_async8(stg + v * P + tid, up + v * ncell + cidx);
+                    if (a != 0.0) cp_async8(stg + (NV + v) * P + tid, A.un + v * ncell + cidx);
+                }
+                cp_async_commit();
+            } else {
+#pragma unroll
+                for (int v = 0; v < NV; v++) {
+                    u0v[v] = __ldg(up + v * ncell + cidx);
+                    unv[v] = a != 0.0 ? __ldg(A.un + v * ncell + cidx) : 0.0;
+                }
             }
         }
         if (live) {
@@ -254,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
         }
         // edge states from the halo cells: one (cell, variable) item per thread
         // round so the extra work spreads over all warps
-        for (int qv = tid; qv < nbr * NV; qv += blockDim.x) {
+        for (int qv = tid - wbeg; qv >= 0 && qv < nbr * NV; qv += wstep) {
             const int v = qv / nbr, q = qv - v * nbr;
             const bool xd = q < 2 * nb1;
             const int qq = xd ? q : q - 2 * nb1;
@@ -327,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
                 for (int v = 0; v < NV; v++) zhi[v] = zhn[v];
             }
         }
-        for (int q = tid; q < nbf; q += blockDim.x) {
+        for (int q = tid - wbeg; q >= 0 && q < nbf; q += wstep) {
             if (q < nb1) xface(q, 0);
             else yface(q - nb1, 0);
         }
@@ -347,7 +385,16 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
                     if (NDIM == 2) L = -(dfx + dfy);
                     else L = -(dfx + dfy) - (fzhi[v] - fzlo[v]) * g.rdx[2];
                 }
-                const double uo = fma(bco, fma(dt, L, u0v[v]), a * unv[v]);
+                double u0, unn;
+                if (STAGE_OPS) {
+                    if (v == 0) cp_async_wait_all();
+                    u0 = stg[v * P + tid];
+                    unn = a != 0.0 ? stg[(NV + v) * P + tid] : 0.0;
+                } else {
+                    u0 = u0v[v];
+                    unn = unv[v];
+                }
+                const double uo = fma(bco, fma(dt, L, u0), a * unn);
                 A.uout[v * ncell + idx] = uo;
                 un[v] = uo;
                 fzlo[v] = fzhi[v];
@@ -378,7 +425,7 @@ cudaError_t launch_t(const StageArgs& a, cudaStream_t s) {
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
     const long long nblk = (long long)a.g.bn[0] * a.g.bn[1] * a.g.bn[2];
-    k<<<(unsigned)nblk, stage_block_threads(a.g), smem, s>>>(a);
+    k<<<(unsigned)nblk, stage_block_threads(a.g, RECON), smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -398,8 +445,9 @@ cudaError_t launch_d(const StageArgs& a, int recon, int riemann, cudaStream_t s)
 
 }  // namespace
 
-int stage_block_threads(const Geo& g) {
+int stage_block_threads(const Geo& g, int recon) {
     const int P = g.nb[0] * (g.ndim >= 2 ? g.nb[1] : 1);
+    if (g.ndim >= 2 && g.nb[0] == 16 && g.nb[1] == 16) return policy_block(g.ndim, recon, 16, 16);
     return ((P + 31) / 32) * 32;
 }
 
@@ -414,7 +462,9 @@ size_t stage_smem_bytes(const Geo& g, int recon) {
     const size_t cur = NV * cw * ch;
     const size_t fx = 2 * NV * (size_t)(nb0 + 1) * nb1;
     const size_t fy = g.ndim >= 2 ? 2 * NV * (size_t)nb0 * (nb1 + 1) : 0;
-    return (ring + cur + fx + fy) * sizeof(double);
+    const bool k16 = g.ndim >= 2 && nb0 == 16 && nb1 == 16;
+    const size_t stg = k16 && policy_stage_ops(g.ndim, recon, 16, 16) ? 2 * NV * P : 0;
+    return (ring + cur + fx + fy + stg) * sizeof(double);
 }
 
 cudaError_t launch_stage(const StageArgs& a, int recon, int riemann, cudaStream_t s) {
