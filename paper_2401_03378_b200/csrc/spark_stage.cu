@@ -36,19 +36,14 @@ using namespace dev;
 constexpr int kThreads = 256;
 
 // Launch policy of a specialisation (host and device agree through this).
-//   stage_ops:      the S4 operands U^(s-1), U^n of the plane are copied to
-//                   shared memory with cp.async (no registers held across S2/S3)
-//   boundary_warp:  a 9th warp does all boundary work (halo loads, halo-cell
-//                   reconstruction, block-boundary faces) so the 8 column warps'
-//                   phases are balanced; needs <= 112 registers (2 CTAs/SM)
+//   stage_ops: the S4 operands U^(s-1), U^n of the plane are copied to shared
+//   memory with cp.async, so no registers are held across S2/S3 (3-D PLM and
+//   first order: their shared-memory budget leaves room for the 20 KiB; WENO5
+//   does not and prefetches into registers).
+// (A 9th "boundary" warp doing all halo work was measured slower in 2-D and
+// 3-D — register cap 112 and a serial boundary critical path — DESIGN.md §4.2.)
 __host__ __device__ constexpr bool policy_stage_ops(int ndim, int recon, int nbx, int nby) {
     return nbx == 16 && nby == 16 && ndim == 3 && recon <= 1;
-}
-__host__ __device__ constexpr bool policy_boundary_warp(int ndim, int recon, int nbx, int nby) {
-    return nbx == 16 && nby == 16 && ndim == 2 && recon >= 0;
-}
-__host__ __device__ constexpr int policy_block(int ndim, int recon, int nbx, int nby) {
-    return policy_boundary_warp(ndim, recon, nbx, nby) ? kThreads + 32 : kThreads;
 }
 
 template <int NV>
@@ -65,9 +60,8 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 template <int NDIM, int RECON, int RS, int NBX, int NBY>
-__global__ void __launch_bounds__(policy_block(NDIM, RECON, NBX, NBY), 2) stage_kernel(const StageArgs A) {
+__global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
     constexpr bool STAGE_OPS = policy_stage_ops(NDIM, RECON, NBX, NBY);
-    constexpr bool BW = policy_boundary_warp(NDIM, RECON, NBX, NBY);
     constexpr int NV = NDIM + 2;
     constexpr int NG = StencilOf<RECON>::NG;
     constexpr int R = NG - 1;  // cell-centric reconstruction radius
@@ -196,9 +190,6 @@ __global__ void __launch_bounds__(policy_block(NDIM, RECON, NBX, NBY), 2) stage_
         }
     }
 
-    // boundary work items: the boundary warp (tid >= 256) or all threads
-    const int wbeg = BW ? kThreads : 0;
-    const int wstep = BW ? 32 : (int)blockDim.x;
     const int nhx = 2 * NG * nb1;
     const int nh = nhx + (NDIM >= 2 ? 2 * NG * nb0 : 0);
     const int nbr = 2 * nb1 + (NDIM >= 2 ? 2 * nb0 : 0);  // boundary recon items
@@ -229,7 +220,7 @@ __global__ void __launch_bounds__(policy_block(NDIM, RECON, NBX, NBY), 2) stage_
 #pragma unroll
             for (int v = 0; v < NV; v++) cur[v * CP + (tj + RO) * cw + ti + NG] = w[v];
         }
-        for (int h = tid - wbeg; h >= 0 && h < nh; h += wstep) {
+        for (int h = tid; h < nh; h += blockDim.x) {
             int cx, cy;
             if (h < nhx) {  // x strips [side][row][depth]
                 const int side = h / (NG * nb1), r = h % (NG * nb1);
@@ -292,7 +283,7 @@ __global__ void __launch_bounds__(policy_block(NDIM, RECON, NBX, NBY), 2) stage_
         }
         // edge states from the halo cells: one (cell, variable) item per thread
         // round so the extra work spreads over all warps
-        for (int qv = tid - wbeg; qv >= 0 && qv < nbr * NV; qv += wstep) {
+        for (int qv = tid; qv < nbr * NV; qv += blockDim.x) {
             const int v = qv / nbr, q = qv - v * nbr;
             const bool xd = q < 2 * nb1;
             const int qq = xd ? q : q - 2 * nb1;
@@ -365,7 +356,7 @@ __global__ void __launch_bounds__(policy_block(NDIM, RECON, NBX, NBY), 2) stage_
                 for (int v = 0; v < NV; v++) zhi[v] = zhn[v];
             }
         }
-        for (int q = tid - wbeg; q >= 0 && q < nbf; q += wstep) {
+        for (int q = tid; q < nbf; q += blockDim.x) {
             if (q < nb1) xface(q, 0);
             else yface(q - nb1, 0);
         }
@@ -445,9 +436,8 @@ cudaError_t launch_d(const StageArgs& a, int recon, int riemann, cudaStream_t s)
 
 }  // namespace
 
-int stage_block_threads(const Geo& g, int recon) {
+int stage_block_threads(const Geo& g, int /*recon*/) {
     const int P = g.nb[0] * (g.ndim >= 2 ? g.nb[1] : 1);
-    if (g.ndim >= 2 && g.nb[0] == 16 && g.nb[1] == 16) return policy_block(g.ndim, recon, 16, 16);
     return ((P + 31) / 32) * 32;
 }
 
