@@ -196,6 +196,33 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
     const int nbf = nb1 + (NDIM >= 2 ? nb0 : 0);          // boundary faces (x face 0, y face 0)
     double cflmin = INFINITY;
 
+    // x/y face-halo cell h of a plane -> block-local (cx, cy):
+    // x strips [side][row][depth], then y strips [side][depth][col]
+    auto halo_cell = [&](int h, int& cx, int& cy) {
+        if (h < nhx) {
+            const int side = h / (NG * nb1), r = h % (NG * nb1);
+            cy = r / NG;
+            const int dp = r % NG;
+            cx = side ? nb0 + dp : dp - NG;
+        } else {
+            const int hh = h - nhx;
+            const int side = hh / (NG * nb0), r = hh % (NG * nb0);
+            const int dp = r / nb0;
+            cx = r % nb0;
+            cy = side ? nb1 + dp : dp - NG;
+        }
+    };
+    // 16x16 planes: nh <= 256, so thread h owns halo cell h for every plane and
+    // prefetches it one plane ahead (raw conserved values in registers)
+    constexpr bool HPF = NBX == 16 && NBY == 16;
+    const bool hact = HPF && tid < nh;
+    int hcx = 0, hcy = 0;
+    double hpre[NV];
+    if (hact) {
+        halo_cell(tid, hcx, hcy);
+        load_cons(hcx, hcy, 0, hpre);
+    }
+
     // raw conserved values of this column's plane kk+NG, loaded one plane ahead
     double pre[NV];
     if (NDIM == 3 && live) load_cons(ti, tj, NG, pre);
@@ -220,24 +247,23 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
 #pragma unroll
             for (int v = 0; v < NV; v++) cur[v * CP + (tj + RO) * cw + ti + NG] = w[v];
         }
-        for (int h = tid; h < nh; h += blockDim.x) {
-            int cx, cy;
-            if (h < nhx) {  // x strips [side][row][depth]
-                const int side = h / (NG * nb1), r = h % (NG * nb1);
-                cy = r / NG;
-                const int dp = r % NG;
-                cx = side ? nb0 + dp : dp - NG;
-            } else {  // y strips [side][depth][col]
-                const int hh = h - nhx;
-                const int side = hh / (NG * nb0), r = hh % (NG * nb0);
-                const int dp = r / nb0;
-                cx = r % nb0;
-                cy = side ? nb1 + dp : dp - NG;
-            }
-            double w[NV];
-            load_prim(cx, cy, kk, w);
+        if (HPF) {  // one halo cell per thread, prefetched one plane ahead
+            if (hact) {
+                double w[NV];
+                ok &= cons_to_prim<NV>(hpre, w, gm1);
+                if (kk + 1 < nb2) load_cons(hcx, hcy, kk + 1, hpre);
 #pragma unroll
-            for (int v = 0; v < NV; v++) cur[v * CP + (cy + RO) * cw + cx + NG] = w[v];
+                for (int v = 0; v < NV; v++) cur[v * CP + (hcy + RO) * cw + hcx + NG] = w[v];
+            }
+        } else {
+            for (int h = tid; h < nh; h += blockDim.x) {
+                int cx, cy;
+                halo_cell(h, cx, cy);
+                double w[NV];
+                load_prim(cx, cy, kk, w);
+#pragma unroll
+                for (int v = 0; v < NV; v++) cur[v * CP + (cy + RO) * cw + cx + NG] = w[v];
+            }
         }
         __syncthreads();
         // ---------------------------------------------------------------- S2
