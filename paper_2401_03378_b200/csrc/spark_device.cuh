@@ -160,6 +160,19 @@ __host__ __device__ __forceinline__ void recon_cell(const double* s, double& lo,
     }
 }
 
+// |u|^2 = (u_x^2 + u_y^2) + u_z^2: symmetric in u_x <-> u_y (bitwise), so a
+// face solved with swapped x/y components gives the identical flux.
+template <int NV>
+__host__ __device__ __forceinline__ double vsq(const double* w) {
+    if (NV == 3) return w[1] * w[1];
+#ifdef __CUDA_ARCH__
+    const double xy = __dadd_rn(__dmul_rn(w[1], w[1]), __dmul_rn(w[2], w[2]));  // never contracted
+#else
+    const double xy = w[1] * w[1] + w[2] * w[2];
+#endif
+    return NV == 5 ? fma(w[3], w[3], xy) : xy;
+}
+
 // ------------------------------------------------------------- Riemann
 // HLL / HLLC (Toro §10.4), Davis wave speeds.  States and flux in the
 // unrotated primitive / conserved order; D is the face normal.  HLLC evaluates
@@ -187,9 +200,7 @@ __host__ __device__ __forceinline__ void riemann(const double* wl, const double*
         const double sk = left ? sl : sr, qk = left ? ql : qr;
         const double rho = w[0], un = w[N], p = w[NV - 1];
         const double irho = rcp(rho);
-        double u2 = 0.0;
-#pragma unroll
-        for (int d = 1; d < NV - 1; d++) u2 = fma(w[d], w[d], u2);
+        const double u2 = vsq<NV>(w);
         const double E = fma(0.5 * rho, u2, p * gm1i);
         const double mflux = rho * un;
         f[0] = mflux;
@@ -197,21 +208,25 @@ __host__ __device__ __forceinline__ void riemann(const double* wl, const double*
         for (int d = 1; d < NV - 1; d++) f[d] = mflux * w[d];
         f[N] += p;
         f[NV - 1] = un * (E + p);
-        if (!lpos && !rneg) {
+        // star-state correction F*_K = F_K + S_K (U*_K - U_K), applied by select
+        // (branch-free, so independent faces interleave; a discarded value may be
+        // non-finite for supersonic faces, which the select never propagates)
+        {
+            const bool star = !lpos && !rneg;
             const double fac = qk * rcp(sk - sstar);
             const double es = fma(sstar - un, fma(p, rcp(qk), sstar), E * irho);
-            f[0] = fma(sk, fac - rho, f[0]);
+            const double c0 = fma(sk, fac - rho, f[0]);
+            f[0] = star ? c0 : f[0];
 #pragma unroll
-            for (int d = 1; d < NV - 1; d++) f[d] = fma(sk, fma(fac, d == N ? sstar : w[d], -rho * w[d]), f[d]);
-            f[NV - 1] = fma(sk, fma(fac, es, -E), f[NV - 1]);
+            for (int d = 1; d < NV - 1; d++) {
+                const double cd = fma(sk, fma(fac, d == N ? sstar : w[d], -rho * w[d]), f[d]);
+                f[d] = star ? cd : f[d];
+            }
+            const double ce = fma(sk, fma(fac, es, -E), f[NV - 1]);
+            f[NV - 1] = star ? ce : f[NV - 1];
         }
     } else {
-        double u2l = 0.0, u2r = 0.0;
-#pragma unroll
-        for (int d = 1; d < NV - 1; d++) {
-            u2l = fma(wl[d], wl[d], u2l);
-            u2r = fma(wr[d], wr[d], u2r);
-        }
+        const double u2l = vsq<NV>(wl), u2r = vsq<NV>(wr);
         const double El = fma(0.5 * rl, u2l, pl * gm1i), Er = fma(0.5 * rr, u2r, pr * gm1i);
         const double ml = rl * ul, mr = rr * ur;
         double UL[NV], UR[NV], FL[NV], FR[NV];

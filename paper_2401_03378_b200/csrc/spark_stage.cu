@@ -60,8 +60,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 template <int NDIM, int RECON, int RS, int NBX, int NBY>
-__global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
+__global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(const StageArgs A) {
     constexpr bool STAGE_OPS = policy_stage_ops(NDIM, RECON, NBX, NBY);
+    constexpr bool FUSE = NBX == 16 && NBY == 16 && NDIM == 3;  // paired face solves (S3)
     constexpr int NV = NDIM + 2;
     constexpr int NG = StencilOf<RECON>::NG;
     constexpr int R = NG - 1;  // cell-centric reconstruction radius
@@ -373,18 +374,113 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(const StageArgs A) {
 #pragma unroll
             for (int v = 0; v < NV; v++) YA[v * fyn + f * nb0 + r] = fl[v];
         };
-        if (live) {
-            xface(tj, ti + 1);
-            if (NDIM >= 2) yface(ti, tj + 1);
+        if (FUSE) {
+            // 16x16 planes: the two independent solves of each round are issued
+            // back to back (branch-free Riemann) so their dependency chains
+            // interleave.  Round 1: own x face + own y face.  Round 2: own z face
+            // and, on warp 0, the 32 block-boundary faces (x face 0 of rows 0-15
+            // on lanes 0-15, y face 0 of columns 0-15 on lanes 16-31, the latter
+            // solved in the x frame with u_x <-> u_y swapped: bitwise identical).
+            const int xo = tj * fxs + ti + 1, yo = (tj + 1) * nb0 + ti;
+            double xl[NV], xr[NV], yl[NV], yr[NV], fx[NV], fy[NV];
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                xl[v] = XA[v * fxn + xo];
+                xr[v] = XB[v * fxn + xo];
+                yl[v] = YA[v * fyn + yo];
+                yr[v] = YB[v * fyn + yo];
+            }
+            if (RECON != 0) {
+                const bool nx = !(positive(xl[0]) && positive(xl[NV - 1]) && positive(xr[0]) && positive(xr[NV - 1]));
+                const bool ny = !(positive(yl[0]) && positive(yl[NV - 1]) && positive(yr[0]) && positive(yr[NV - 1]));
+                if (__any_sync(0xffffffffu, nx || ny)) {
+#pragma unroll
+                    for (int v = 0; v < NV; v++) {
+                        if (nx) {
+                            xl[v] = cur[v * CP + (tj + RO) * cw + ti + NG];
+                            xr[v] = cur[v * CP + (tj + RO) * cw + ti + 1 + NG];
+                        }
+                        if (ny) {
+                            yl[v] = cur[v * CP + (tj + NG) * cw + ti + NG];
+                            yr[v] = cur[v * CP + (tj + 1 + NG) * cw + ti + NG];
+                        }
+                    }
+                }
+            }
+            riemann<NV, RS, 0>(xl, xr, gamma, gm1i, fx);
+            riemann<NV, RS, 1>(yl, yr, gamma, gm1i, fy);
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                XA[v * fxn + xo] = fx[v];
+                YA[v * fyn + yo] = fy[v];
+            }
+            // round 2
+            if (NDIM == 3 && RECON != 0) {
+                const bool nz = !(positive(zhi[0]) && positive(zhi[NV - 1]) && positive(zlo[0]) && positive(zlo[NV - 1]));
+                if (__any_sync(0xffffffffu, nz) && nz) {
+#pragma unroll
+                    for (int v = 0; v < NV; v++) {
+                        zhi[v] = ring_at(kk, v);
+                        zlo[v] = ring_at(kk + 1, v);
+                    }
+                }
+            }
+            if (tid < 32) {  // warp 0: boundary face (+ its z faces)
+                const bool isy = tid >= 16;
+                const int q = tid & 15;
+                double bl[NV], br[NV], fb[NV];
+#pragma unroll
+                for (int v = 0; v < NV; v++) {
+                    bl[v] = isy ? YA[v * fyn + q] : XA[v * fxn + q * fxs];
+                    br[v] = isy ? YB[v * fyn + q] : XB[v * fxn + q * fxs];
+                }
+                if (RECON != 0 && !(positive(bl[0]) && positive(bl[NV - 1]) && positive(br[0]) && positive(br[NV - 1]))) {
+#pragma unroll
+                    for (int v = 0; v < NV; v++) {
+                        bl[v] = isy ? cur[v * CP + (NG - 1) * cw + q + NG] : cur[v * CP + (q + RO) * cw + NG - 1];
+                        br[v] = isy ? cur[v * CP + NG * cw + q + NG] : cur[v * CP + (q + RO) * cw + NG];
+                    }
+                }
+                {  // y faces in the x frame
+                    const double l1 = bl[1], r1 = br[1];
+                    bl[1] = isy ? bl[2] : l1;
+                    bl[2] = isy ? l1 : bl[2];
+                    br[1] = isy ? br[2] : r1;
+                    br[2] = isy ? r1 : br[2];
+                }
+                if (NDIM == 3) riemann<NV, RS, 2>(zhi, zlo, gamma, gm1i, fzhi);
+                riemann<NV, RS, 0>(bl, br, gamma, gm1i, fb);
+                {
+                    const double f1 = fb[1];
+                    fb[1] = isy ? fb[2] : f1;
+                    fb[2] = isy ? f1 : fb[2];
+                }
+#pragma unroll
+                for (int v = 0; v < NV; v++) {
+                    if (isy) YA[v * fyn + q] = fb[v];
+                    else XA[v * fxn + q * fxs] = fb[v];
+                }
+            } else if (NDIM == 3) {
+                riemann<NV, RS, 2>(zhi, zlo, gamma, gm1i, fzhi);
+            }
             if (NDIM == 3) {
-                zflux(kk, zhi, zlo, fzhi);
 #pragma unroll
                 for (int v = 0; v < NV; v++) zhi[v] = zhn[v];
             }
-        }
-        for (int q = tid; q < nbf; q += blockDim.x) {
-            if (q < nb1) xface(q, 0);
-            else yface(q - nb1, 0);
+        } else {
+            if (live) {
+                xface(tj, ti + 1);
+                if (NDIM >= 2) yface(ti, tj + 1);
+                if (NDIM == 3) {
+                    zflux(kk, zhi, zlo, fzhi);
+#pragma unroll
+                    for (int v = 0; v < NV; v++) zhi[v] = zhn[v];
+                }
+            }
+            for (int q = tid; q < nbf; q += blockDim.x) {
+                if (q < nb1) xface(q, 0);
+                else yface(q - nb1, 0);
+            }
         }
         __syncthreads();
         // ---------------------------------------------------------------- S4
