@@ -122,7 +122,10 @@ spark_status spark_required_bytes(const spark_config* cfg, int32_t rank, int32_t
 /* Rank 0 creates the NCCL unique id (128 bytes); the harness broadcasts it. */
 spark_status spark_nccl_unique_id(uint8_t id[128]);
 
-/* Create a context on CUDA device `device`.  nranks == 1: nccl_id may be NULL.
+/* Create a context on CUDA device `device`.  nranks == 1: nccl_id may be NULL;
+ * a non-NULL id selects self-exchange mode (periodic faces are packed and sent
+ * to this rank itself with NCCL send/recv instead of the local wrap — the
+ * multi-rank exchange path on one GPU, for testing; results are bitwise equal).
  * nranks > 1: nccl_id from spark_nccl_unique_id on rank 0 (collective call:
  * every rank must call spark_init).  cuda_stream is a cudaStream_t (NULL =
  * legacy default stream).  arena: device memory of >= required bytes, owned

@@ -119,7 +119,10 @@ struct Plan {
     spark::Geo geo;
 };
 
-Plan make_plan(const spark_config* c, int rank, int nranks) {
+// self_exchange: periodic dims owned entirely by this rank are still exchanged
+// through the halo path (peer = self) — used with a 1-rank NCCL communicator to
+// exercise pack + NCCL send/recv + slab reads on a single GPU.
+Plan make_plan(const spark_config* c, int rank, int nranks, bool self_exchange = false) {
     std::string m = check(c, nranks);
     if (!m.empty()) throw Error(SPARK_ERR_ARG, m);
     if (rank < 0 || rank >= nranks) throw Error(SPARK_ERR_ARG, "rank out of range");
@@ -157,7 +160,8 @@ Plan make_plan(const spark_config* c, int rank, int nranks) {
             int q[3] = {p.pc[0], p.pc[1], p.pc[2]};
             q[d] += s ? 1 : -1;
             if (q[d] < 0 || q[d] >= p.pg[d]) {
-                if (c->bc[d][s] != SPARK_BC_PERIODIC || p.pg[d] == 1) continue;  // local boundary map
+                if (c->bc[d][s] != SPARK_BC_PERIODIC) continue;  // physical boundary: local map
+                if (p.pg[d] == 1 && !self_exchange) continue;     // periodic self-wrap: local map
                 q[d] = (q[d] + p.pg[d]) % p.pg[d];
             }
             p.peer[d][s] = q[0] + p.pg[0] * (q[1] + p.pg[1] * q[2]);
@@ -272,14 +276,14 @@ void carve(spark_ctx* c, void* arena, size_t bytes) {
 }
 
 spark_ctx* make_ctx(const spark_config* cfg, int rank, int nranks, int device, void* stream, void* arena,
-                    size_t bytes) {
+                    size_t bytes, bool self_exchange = false) {
     auto c = std::make_unique<spark_ctx>();
     c->cfg = *cfg;
     c->rank = rank;
     c->nranks = nranks;
     c->device = device;
     c->stream = static_cast<cudaStream_t>(stream);
-    c->plan = make_plan(cfg, rank, nranks);
+    c->plan = make_plan(cfg, rank, nranks, self_exchange);
     carve(c.get(), arena, bytes);
     set_device(c.get());
     launched(c.get(), spark::launch_scalars_reset(c->sc, c->stream), "scalars reset");
@@ -327,7 +331,7 @@ void exchange_local(const std::vector<spark_ctx*>& m) {
 }
 
 void allreduce_acc(spark_ctx* c) {
-    if (c->nranks > 1 && c->comm)
+    if (c->comm)
         NC(ncclAllReduce(&c->sc->acc, &c->sc->acc, 1, ncclUint64, ncclMin, c->comm, c->stream));
 }
 
@@ -429,7 +433,7 @@ void do_step(spark_ctx* c, double dt) {
         newn = stage_buffers(S, c->n_idx, s, &pi, &po);
         double a, b;
         rk_coeffs(S, s, &a, &b);
-        if (c->nranks > 1) {
+        if (c->comm) {
             pack_all(c, c->U[pi]);
             exchange_nccl(c);
         }
@@ -505,7 +509,8 @@ spark_status spark_halo_plan(const spark_config* cfg, int32_t rank, int32_t nran
 spark_status spark_required_bytes(const spark_config* cfg, int32_t rank, int32_t nranks, size_t* bytes) {
     return guard(nullptr, [&] {
         if (!bytes) throw Error(SPARK_ERR_ARG, "null bytes");
-        *bytes = arena_bytes(make_plan(cfg, rank, nranks));
+        // one rank: room for the self-exchange slabs too (periodic dims, spark_init with an NCCL id)
+        *bytes = arena_bytes(make_plan(cfg, rank, nranks, nranks == 1));
     });
 }
 
@@ -525,8 +530,12 @@ spark_status spark_init(const spark_config* cfg, int32_t rank, int32_t nranks, c
     spark_ctx* made = nullptr;
     spark_status st = guard(nullptr, [&] {
         if (nranks > 1 && !nccl_id) throw Error(SPARK_ERR_ARG, "nranks > 1 needs an NCCL id");
-        std::unique_ptr<spark_ctx> c(make_ctx(cfg, rank, nranks, device, cuda_stream, arena, arena_bytes_));
-        if (nranks > 1) {
+        // nranks == 1 with an NCCL id: periodic faces go through pack + NCCL
+        // send/recv to self (exercises the multi-rank exchange on one GPU)
+        const bool self_exchange = nranks == 1 && nccl_id;
+        std::unique_ptr<spark_ctx> c(
+            make_ctx(cfg, rank, nranks, device, cuda_stream, arena, arena_bytes_, self_exchange));
+        if (nccl_id) {
             ncclUniqueId u;
             std::memcpy(&u, nccl_id, 128);
             NC(ncclCommInitRank(&c->comm, nranks, u, rank));
@@ -660,7 +669,7 @@ spark_status spark_fill_guardcells(spark_ctx* ctx, double* padded_out) {
         if (ctx->group) {
             for (spark_ctx* m : ctx->group->members) pack_all(m, m->U[m->n_idx]);
             exchange_local(ctx->group->members);
-        } else if (ctx->nranks > 1) {
+        } else if (ctx->comm) {
             pack_all(ctx, ctx->U[ctx->n_idx]);
             exchange_nccl(ctx);
         }
@@ -769,7 +778,8 @@ spark_status spark_stage_apply(spark_ctx* ctx, const double* U_prev, const doubl
                                double* U_out) {
     if (!ctx || !U_prev || !U_out) return SPARK_ERR_ARG;
     return guard(ctx, [&] {
-        if (ctx->nranks != 1) throw Error(SPARK_ERR_STATE, "spark_stage_apply needs a single-rank context");
+        if (ctx->nranks != 1 || ctx->comm)
+            throw Error(SPARK_ERR_STATE, "spark_stage_apply needs a single-rank context without NCCL exchange");
         if (a != 0.0 && !U_n) throw Error(SPARK_ERR_ARG, "U_n required when a != 0");
         set_device(ctx);
         stage_launch(ctx, U_prev, U_n, a, b, U_out, false, nullptr, dt, false);

@@ -350,3 +350,32 @@ def test_errors(sp):
         s.step()
     with pytest.raises(sp.SparkError):
         sp.Spark(p.with_(ng=1).config())
+
+
+@pytest.mark.parametrize("p", [
+    si.Problem("s3", 3, (16, 16, 16), (2, 2, 2), 3, 2, 1, 3, 0.3, bc=((0, 0), (0, 0), (0, 0))),
+    si.Problem("s3m", 3, (8, 8, 8), (2, 3, 2), 2, 1, 1, 2, 0.3, bc=((0, 0), (1, 2), (0, 0))),
+    si.Problem("s2", 2, (16, 16, 1), (3, 2, 1), 2, 1, 1, 2, 0.4, bc=((0, 0), (0, 0), (1, 1))),
+], ids=lambda p: p.name)
+def test_nccl_self_exchange_bitwise(sp, p):
+    """One rank with an NCCL communicator: periodic faces go through pack ->
+    ncclSend/ncclRecv (to self, the message order of exchange_nccl) -> KB1 slab
+    reads, plus the dt all-reduce.  Must equal the local-wrap path bit for bit."""
+    U0 = cons(p, si.random_state(p, 17, blocky=True))
+    plain = make(sp, p, U=U0)
+    viaccl = sp.Spark(p.config(), nccl_id=sp.nccl_unique_id())
+    viaccl.set_state(U0)
+    for _ in range(3):
+        assert plain.step(sync=True) == viaccl.step(sync=True)
+    assert np.array_equal(state(plain), state(viaccl))
+    # padded blocks: interior and face guards identical; edges/corners that lie
+    # across two exchanged faces are not exchanged (star stencil) and read NaN
+    Pp = plain.fill_guardcells().cpu().numpy()
+    Pn = viaccl.fill_guardcells().cpu().numpy()
+    g = [p.ng if d < p.ndim else 0 for d in range(3)]
+    k, j, i = np.meshgrid(*[np.arange(p.nb[d] + 2 * g[d]) for d in (2, 1, 0)], indexing="ij")
+    outside = sum(((c < g[d]) | (c >= g[d] + p.nb[d])).astype(int) for c, d in ((i, 0), (j, 1), (k, 2)))
+    face = outside <= 1
+    assert np.array_equal(Pp[:, :, face], Pn[:, :, face])
+    assert not np.isnan(Pn[:, :, face]).any()
+    viaccl.close()
