@@ -227,6 +227,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-calibration", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -340,6 +341,29 @@ def main():
                "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
                "note": "per step: spark_set_state from pinned host + spark_step + spark_get_state to pinned host"}
 
+    # ---- same-run HBM calibration: the paper's AXPY mappings (NEXT N4) on
+    # 2^27-element FP64 vectors (1 GiB each, > L2): 24 bytes per element
+    calib = None
+    if not args.no_calibration:
+        n = 1 << 27
+        x = torch.ones(n, dtype=torch.float64, device=f"cuda:{local}")
+        y = torch.zeros(n, dtype=torch.float64, device=f"cuda:{local}")
+        calib = {}
+        with torch.cuda.stream(stream):
+            for var, name in spark.AXPY_VARIANTS.items():
+                for _ in range(2):
+                    spark.axpy(var, 0.5, x, y, stream)
+                c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                c0.record(stream)
+                for _ in range(5):
+                    spark.axpy(var, 0.5, x, y, stream)
+                c1.record(stream)
+                stream.synchronize()
+                calib[name] = 24.0 * n * 5 / (c0.elapsed_time(c1) * 1e-3) / 1e9
+        del x, y
+        roofline["peak_live_axpy"] = max(calib.values())
+        roofline["frac_of_live_axpy"] = achieved / roofline["peak_live_axpy"]
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample = oracle_sample(p, args.cpu_budget)
@@ -355,7 +379,8 @@ def main():
                        "block": list(p.nb), "blocks": list(p.nblk), "recon": ["first", "plm", "weno5"][p.recon],
                        "riemann": ["hll", "hllc"][p.riemann], "rk_stages": p.rk_stages, "ng": p.ng,
                        "parallelism": f"blocks over {world} GPU(s)", "l2": "state per copy > L2 (no flush needed)"},
-            "roofline": roofline, "roofline_fp64": roofline_fp64, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "roofline_fp64": roofline_fp64, "hbm_calibration_gbs": calib,
+            "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": total_launches,
             "clocks": clocks,
         }

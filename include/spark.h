@@ -224,6 +224,19 @@ spark_status spark_profile_enable(spark_ctx* ctx, int32_t on);
 spark_status spark_profile_read(spark_ctx* ctx, double* stage_ms, int64_t* stage_launches,
                                 int64_t* total_launches);
 
+/* ---- HBM calibration -------------------------------------------- */
+
+/* y_i = a x_i + y_i for i < n (FP64, device pointers, no FMA contraction), with
+ * the paper's thread-to-entry mappings (§3.3): variant 0 = increment by 1
+ * (alg:axpy-incr-1: contiguous chunk per thread), 1 = increment by
+ * #threads (alg:axpy-incr-threads: grid stride), 2 = single
+ * iteration (alg:axpy-single-iter: one entry per thread, T >= N),
+ * 3 = B200 vectorised grid stride (16-byte accesses; x, y 16-byte aligned).
+ * Enqueued on cuda_stream (a cudaStream_t) of device `device`; asynchronous.
+ * Used by bench.py as a same-run HBM bandwidth denominator. */
+spark_status spark_axpy(int32_t device, int32_t variant, int64_t n, double a, const double* x, double* y,
+                        void* cuda_stream);
+
 /* ---- self test ----------------------------------------------------------------- */
 
 /* Evaluate the device Riemann solver (the one KB1 calls, calcFlux P:1833) on n

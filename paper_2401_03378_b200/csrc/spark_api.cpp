@@ -855,3 +855,14 @@ extern "C" spark_status spark_selftest_riemann(int32_t device, int32_t riemann, 
         CU(cudaMemcpy(f, df, bytes, cudaMemcpyDeviceToHost));
     });
 }
+
+extern "C" spark_status spark_axpy(int32_t device, int32_t variant, int64_t n, double a, const double* x, double* y,
+                                   void* cuda_stream) {
+    return guard(nullptr, [&] {
+        if (variant < 0 || variant > 3 || n < 0 || (n > 0 && (!x || !y))) throw Error(SPARK_ERR_ARG, "bad axpy arguments");
+        CU(cudaSetDevice(device));
+        int sms = 0;
+        CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        CU(spark::launch_axpy(variant, n, a, x, y, sms, static_cast<cudaStream_t>(cuda_stream)));
+    });
+}

@@ -71,6 +71,7 @@ cudaError_t launch_scalars_reset(DevScalars* sc, cudaStream_t s);
 cudaError_t launch_group_min(const AccPtrs& p, int n, cudaStream_t s);
 cudaError_t launch_selftest_riemann(int riemann, int ndim, int dir, double gamma, int64_t n, const double* wl,
                                     const double* wr, double* f);
+cudaError_t launch_axpy(int variant, int64_t n, double a, const double* x, double* y, int sms, cudaStream_t s);
 size_t stage_smem_bytes(const Geo& g, int recon);
 int stage_block_threads(const Geo& g, int recon);
 

@@ -269,3 +269,61 @@ cudaError_t launch_selftest_riemann(int riemann, int ndim, int dir, double gamma
     return riemann ? st_d<5, 1>(dir, n, gamma, wl, wr, f) : st_d<5, 0>(dir, n, gamma, wl, wr, f);
 }
 }  // namespace spark
+
+// ---------------------------------------------------------- AXPY (NEXT N4)
+// The paper's AXPY thread mappings (alg:axpy-incr-1 P:1041-1060,
+// alg:axpy-incr-threads P:1061-1079, alg:axpy-single-iter P:1086-1100) as an
+// in-run HBM calibration: y_i = a x_i + y_i in FP64, never FMA-contracted
+// (bitwise equal to a separate multiply and add).  Variant 3 is the B200 form:
+// 16-byte vector accesses, grid = a multiple of the SM count.
+namespace spark {
+namespace {
+__device__ __forceinline__ double axpy1(double a, double x, double y) { return __dadd_rn(__dmul_rn(a, x), y); }
+
+__global__ void axpy_incr_1(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t lo = (n * t) / T, hi = (n * (t + 1)) / T;  // floor(N t / T), floor(N (t+1) / T)
+    for (int64_t i = lo; i < hi; i++) y[i] = axpy1(a, x[i], y[i]);
+}
+
+__global__ void axpy_incr_threads(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, T = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = t; i < n; i += T) y[i] = axpy1(a, x[i], y[i]);
+}
+
+__global__ void axpy_single_iter(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) y[i] = axpy1(a, x[i], y[i]);
+}
+
+__global__ void axpy_vec2(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n2 = n / 2;
+    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
+    double2* __restrict__ y2 = reinterpret_cast<double2*>(y);
+    for (int64_t i = t; i < n2; i += T) {
+        const double2 xv = __ldcs(x2 + i);
+        double2 yv = __ldcs(y2 + i);
+        yv.x = axpy1(a, xv.x, yv.x);
+        yv.y = axpy1(a, xv.y, yv.y);
+        __stcs(y2 + i, yv);
+    }
+    if (t == 0 && (n & 1)) y[n - 1] = axpy1(a, x[n - 1], y[n - 1]);
+}
+}  // namespace
+
+cudaError_t launch_axpy(int variant, int64_t n, double a, const double* x, double* y, int sms, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int threads = 256;
+    const unsigned persistent = (unsigned)(sms * 8);  // 8 x 256-thread CTAs per SM
+    switch (variant) {
+        case 0: axpy_incr_1<<<persistent, threads, 0, s>>>(n, a, x, y); break;
+        case 1: axpy_incr_threads<<<persistent, threads, 0, s>>>(n, a, x, y); break;
+        case 2: axpy_single_iter<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(n, a, x, y); break;
+        default:
+            if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) return cudaErrorInvalidValue;
+            axpy_vec2<<<persistent, threads, 0, s>>>(n, a, x, y);
+    }
+    return cudaGetLastError();
+}
+}  // namespace spark

@@ -25,7 +25,7 @@ EXPORTS = [
     "spark_finalize", "spark_last_error", "spark_set_state", "spark_set_primitive", "spark_get_state",
     "spark_get_time", "spark_get_cfl_min", "spark_fill_guardcells", "spark_step", "spark_advance",
     "spark_step_group", "spark_stage_apply", "spark_profile_enable", "spark_profile_read",
-    "spark_selftest_riemann",
+    "spark_selftest_riemann", "spark_axpy",
 ]
 
 
@@ -120,6 +120,7 @@ def lib() -> ctypes.CDLL:
         "spark_profile_enable": (i32, [vp, i32]),
         "spark_profile_read": (i32, [vp, P(d), P(i64), P(i64)]),
         "spark_selftest_riemann": (i32, [i32, i32, i32, i32, d, i64, P(d), P(d), P(d)]),
+        "spark_axpy": (i32, [i32, i32, i64, d, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -190,6 +191,21 @@ def selftest_riemann(kind: int, ndim: int, direction: int, gamma: float, wl: np.
     _check(lib().spark_selftest_riemann(device, kind, ndim, direction, gamma, wl.shape[0], dp(wl), dp(wr), dp(f)),
            what="selftest_riemann")
     return f
+
+
+AXPY_VARIANTS = {0: "axpy_increment_1", 1: "axpy_increment_threads", 2: "axpy_single_iter", 3: "axpy_vec2"}
+
+
+def axpy(variant: int, a: float, x, y, stream=None):
+    """y <- a x + y on the device (torch float64 CUDA tensors), paper AXPY mapping `variant`."""
+    import torch
+
+    assert x.dtype == torch.float64 and y.dtype == torch.float64 and x.is_cuda and y.is_cuda
+    assert x.numel() == y.numel() and x.is_contiguous() and y.is_contiguous()
+    st = stream if stream is not None else torch.cuda.current_stream(y.device)
+    _check(lib().spark_axpy(y.device.index, variant, y.numel(), a, ctypes.c_void_p(x.data_ptr()),
+                            ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(st.cuda_stream)), what="axpy")
+    return y
 
 
 def local_shape(cfg: dict, rank: int = 0, nranks: int = 1):

@@ -379,3 +379,16 @@ def test_nccl_self_exchange_bitwise(sp, p):
     assert np.array_equal(Pp[:, :, face], Pn[:, :, face])
     assert not np.isnan(Pn[:, :, face]).any()
     viaccl.close()
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("n", [1, 1000, 1_000_003])
+def test_axpy_variants(sp, variant, n):
+    """NEXT N4: the paper's AXPY thread mappings (alg:axpy-*) give exactly
+    a*x + y (separate multiply and add, as numpy computes it)."""
+    g = np.random.Generator(np.random.PCG64(n + variant))
+    x, y = g.normal(size=n), g.normal(size=n)
+    a = 0.7310585786300049
+    yd = torch.from_numpy(y.copy()).cuda()
+    sp.axpy(variant, a, torch.from_numpy(x).cuda(), yd)
+    assert np.array_equal(yd.cpu().numpy(), a * x + y)
