@@ -208,6 +208,8 @@ struct spark_ctx {
     double* recv[3][2] = {};
     spark::DevScalars* sc = nullptr;
     ncclComm_t comm = nullptr;
+    cudaStream_t comm_stream = nullptr;        // NCCL halo exchange overlaps interior blocks
+    cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
     std::shared_ptr<LocalGroup> group;
     bool have_state = false;
     std::string err;
@@ -302,15 +304,15 @@ void pack_all(spark_ctx* c, const double* u) {
 // halo <- low peer, send low slab -> low peer, recv high halo <- high peer];
 // posting in the same order on every rank matches messages between the same
 // pair of ranks (P_d = 2 periodic: both faces have the same peer).
-void exchange_nccl(spark_ctx* c) {
+void exchange_nccl(spark_ctx* c, cudaStream_t st) {
     const spark::Geo& g = c->plan.geo;
     NC(ncclGroupStart());
     for (int d = 0; d < 3; d++) {
         const size_t n = (size_t)g.nvar * g.slab[d];
-        if (c->plan.peer[d][1] >= 0) NC(ncclSend(c->send[d][1], n, ncclFloat64, c->plan.peer[d][1], c->comm, c->stream));
-        if (c->plan.peer[d][0] >= 0) NC(ncclRecv(c->recv[d][0], n, ncclFloat64, c->plan.peer[d][0], c->comm, c->stream));
-        if (c->plan.peer[d][0] >= 0) NC(ncclSend(c->send[d][0], n, ncclFloat64, c->plan.peer[d][0], c->comm, c->stream));
-        if (c->plan.peer[d][1] >= 0) NC(ncclRecv(c->recv[d][1], n, ncclFloat64, c->plan.peer[d][1], c->comm, c->stream));
+        if (c->plan.peer[d][1] >= 0) NC(ncclSend(c->send[d][1], n, ncclFloat64, c->plan.peer[d][1], c->comm, st));
+        if (c->plan.peer[d][0] >= 0) NC(ncclRecv(c->recv[d][0], n, ncclFloat64, c->plan.peer[d][0], c->comm, st));
+        if (c->plan.peer[d][0] >= 0) NC(ncclSend(c->send[d][0], n, ncclFloat64, c->plan.peer[d][0], c->comm, st));
+        if (c->plan.peer[d][1] >= 0) NC(ncclRecv(c->recv[d][1], n, ncclFloat64, c->plan.peer[d][1], c->comm, st));
     }
     NC(ncclGroupEnd());
 }
@@ -340,7 +342,7 @@ void allreduce_acc(spark_ctx* c) {
 void group_min(const std::vector<spark_ctx*>& m);
 
 void stage_launch(spark_ctx* c, const double* prev, const double* un, double a, double b, double* out,
-                  bool last, const double* dt_ptr, double dt_value, bool honor_active) {
+                  bool last, const double* dt_ptr, double dt_value, bool honor_active, int part = 0) {
     spark::StageArgs A{};
     A.g = c->plan.geo;
     A.uprev = prev;
@@ -355,6 +357,7 @@ void stage_launch(spark_ctx* c, const double* prev, const double* un, double a, 
     A.dt_value = dt_value;
     A.last = last ? 1 : 0;
     A.honor_active = honor_active ? 1 : 0;
+    A.part = part;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->prof) {
         if (c->ev_used == c->ev.size()) {
@@ -369,7 +372,7 @@ void stage_launch(spark_ctx* c, const double* prev, const double* un, double a, 
         CU(cudaEventRecord(e0, c->stream));
     }
     launched(c, spark::launch_stage(A, c->cfg.recon, c->cfg.riemann, c->stream), "stage kernel");
-    c->stage_launches++;
+    if (part != 2) c->stage_launches++;  // a split stage (interior + boundary) counts once
     if (c->prof) CU(cudaEventRecord(e1, c->stream));
 }
 
@@ -434,10 +437,20 @@ void do_step(spark_ctx* c, double dt) {
         double a, b;
         rk_coeffs(S, s, &a, &b);
         if (c->comm) {
+            // pack on the compute stream; the NCCL exchange runs on the comm
+            // stream while the interior blocks (no exchanged face) compute;
+            // the rank-boundary blocks wait for the received slabs
             pack_all(c, c->U[pi]);
-            exchange_nccl(c);
+            CU(cudaEventRecord(c->ev_packed, c->stream));
+            CU(cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
+            exchange_nccl(c, c->comm_stream);
+            CU(cudaEventRecord(c->ev_recv, c->comm_stream));
+            stage_launch(c, c->U[pi], c->U[c->n_idx], a, b, c->U[po], s == S, &c->sc->dt, dt, true, 1);
+            CU(cudaStreamWaitEvent(c->stream, c->ev_recv, 0));
+            stage_launch(c, c->U[pi], c->U[c->n_idx], a, b, c->U[po], s == S, &c->sc->dt, dt, true, 2);
+        } else {
+            stage_launch(c, c->U[pi], c->U[c->n_idx], a, b, c->U[po], s == S, &c->sc->dt, dt, true);
         }
-        stage_launch(c, c->U[pi], c->U[c->n_idx], a, b, c->U[po], s == S, &c->sc->dt, dt, true);
     }
     allreduce_acc(c);
     c->n_idx = newn;
@@ -539,6 +552,9 @@ spark_status spark_init(const spark_config* cfg, int32_t rank, int32_t nranks, c
             ncclUniqueId u;
             std::memcpy(&u, nccl_id, 128);
             NC(ncclCommInitRank(&c->comm, nranks, u, rank));
+            CU(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+            CU(cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&c->ev_recv, cudaEventDisableTiming));
         }
         made = c.release();
     });
@@ -576,7 +592,11 @@ spark_status spark_finalize(spark_ctx* ctx) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
         }
+        if (ctx->comm_stream) CU(cudaStreamSynchronize(ctx->comm_stream));
         if (ctx->comm) ncclCommDestroy(ctx->comm);
+        if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+        if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
+        if (ctx->ev_recv) cudaEventDestroy(ctx->ev_recv);
     });
     if (ctx->group) {
         auto& m = ctx->group->members;
@@ -671,7 +691,7 @@ spark_status spark_fill_guardcells(spark_ctx* ctx, double* padded_out) {
             exchange_local(ctx->group->members);
         } else if (ctx->comm) {
             pack_all(ctx, ctx->U[ctx->n_idx]);
-            exchange_nccl(ctx);
+            exchange_nccl(ctx, ctx->stream);
         }
         if (padded_out) {
             const double* halo[3][2];

@@ -51,6 +51,8 @@ struct StageArgs {
     double dt_value;
     int last;                     // 1: fuse the CFL-min epilogue
     int honor_active;             // 1: copy-through when sc->active == 0
+    int part;                     // 0 all blocks; 1 blocks touching no exchanged rank face
+                                  // ("interior", run while halos travel); 2 the others
 };
 
 constexpr int kMaxGroup = 64;

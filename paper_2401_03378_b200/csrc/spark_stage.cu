@@ -104,6 +104,12 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     const double a = A.a, bco = A.b;
     const double gamma = g.gamma, gm1 = g.gamma - 1.0, gm1i = 1.0 / (g.gamma - 1.0);
 
+    if (A.part) {  // interior / rank-boundary split (CTA-uniform early exit)
+        const bool edge = (g.halo[0][0] && bx == 0) || (g.halo[0][1] && bx == g.bn[0] - 1) ||
+                          (NDIM >= 2 && ((g.halo[1][0] && by == 0) || (g.halo[1][1] && by == g.bn[1] - 1))) ||
+                          (NDIM >= 3 && ((g.halo[2][0] && bz == 0) || (g.halo[2][1] && bz == g.bn[2] - 1)));
+        if (edge != (A.part == 2)) return;
+    }
     if (A.honor_active && !A.sc->active) {  // t >= t_end: U^(s) = U^(s-1)
         if (live)
             for (int kk = 0; kk < nb2; kk++) {
