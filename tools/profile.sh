@@ -2,7 +2,7 @@
 # ncu evidence for the stage kernel (run under gpurun; one GPU).
 # usage: tools/profile.sh TAG [CONFIG]
 TAG=${1:-r1}; CFG=${2:-c4_sedov3d_plm}
-CMD="python bench.py --config $CFG --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+CMD="python bench.py --config $CFG --steps 3 --warmup 3 --no-cpu-baseline --no-calibration --e2e-steps 1"
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain_${TAG}.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > /dev/null 2>&1 && \
