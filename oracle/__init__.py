@@ -87,6 +87,7 @@ def lib():
             "oracle_stage": (i32, [P(_Cfg), dp, dp, d, d, d, dp]),
             "oracle_rk_coeffs": (None, [i32, i32, dp, dp]),
             "oracle_step": (i32, [P(_Cfg), dp, d, d, d, dp]),
+            "oracle_step_telescoping": (i32, [P(_Cfg), dp, d, d, d, dp]),
             "oracle_run": (i32, [P(_Cfg), dp, d, i64, dp, P(ctypes.c_long)]),
             "oracle_num_threads": (i32, []),
         }
@@ -274,6 +275,18 @@ def step(cfg, U, t=0.0, t_end=0.0, dt_fixed=0.0):
     d = ctypes.c_double()
     c = cfg.c()
     _chk(lib().oracle_step(ctypes.byref(c), _dp(U), t, t_end, dt_fixed, ctypes.byref(d)), "step")
+    return U, d.value
+
+
+def step_telescoping(cfg, U, t=0.0, t_end=0.0, dt_fixed=0.0):
+    """One telescoping SSP-RK step: one thick guard fill, all
+    stages per block on the shrinking halo; returns (U_new, dt_used)."""
+    cfg = _as_cfg(cfg)
+    U = np.array(U, dtype=np.float64, copy=True, order="C")
+    d = ctypes.c_double()
+    c = cfg.c()
+    _chk(lib().oracle_step_telescoping(ctypes.byref(c), _dp(U), t, t_end, dt_fixed, ctypes.byref(d)),
+         "step_telescoping")
     return U, d.value
 
 

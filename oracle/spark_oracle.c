@@ -535,3 +535,164 @@ int oracle_num_threads(void) {
     return 1;
 #endif
 }
+
+/* ------------------------------------------------- telescoping SSP-RK (N1) */
+/* Telescoping mode (lst:spark-telescoping P:1598-1604): ONE
+ * fill_guardcells per step with S*NGK guard layers (all guards, edges and
+ * corners included), then for every block all S stages, each updating the
+ * block *and* the part of its halo that the later stages still need: stage s
+ * updates the padded cells at distance >= s*NGK from the tile edge.  NGK is the
+ * reconstruction half-width (1 first order, 2 PLM, 3 WENO5).  Guard cells
+ * beyond a physical boundary are filled from the boundary map once and then
+ * evolved like any halo cell (reading R17).  With periodic boundaries the
+ * result equals the non-telescoping step exactly (same arithmetic on the same
+ * values).  dt as in oracle_step (CFL of U^n). */
+static int ngk_of(int recon) { return recon == OREC_WENO5 ? 3 : (recon == OREC_PLM ? 2 : 1); }
+
+int oracle_step_telescoping(const ocfg* c, double* U, double t, double t_end, double dt_fixed, double* dt_used) {
+    if (oracle_check_config(c)) return OERR_ARG;
+    const int nv = nvar_of(c), ndim = c->ndim, S = c->rk_stages, ngk = ngk_of(c->recon);
+    const int G = S * ngk;
+    ocfg ct = *c;  /* fill with the thick halo */
+    ct.ng = G;
+    for (int d = 0; d < ndim; d++)
+        if (c->nb[d] < 1) return OERR_ARG;
+    const long NB = nblocks(c), nc = cells_per_block(c);
+    int g[3], pn[3];
+    long np = 1;
+    for (int d = 0; d < 3; d++) {
+        g[d] = d < ndim ? G : 0;
+        pn[d] = c->nb[d] + 2 * g[d];
+        np *= pn[d];
+    }
+    const long pstride[3] = {1, pn[0], (long)pn[0] * pn[1]};
+    double dx[3] = {dx_of(c, 0), dx_of(c, 1), dx_of(c, 2)};
+    double dt = dt_fixed > 0.0 ? dt_fixed : oracle_dt(c, U, t, t_end);
+    if (dt_used) *dt_used = dt;
+    /* the thick-halo fill needs N_d >= G for the per-dimension maps */
+    double* P = malloc(sizeof(double) * nv * NB * np);
+    double* Unew = malloc(sizeof(double) * nv * NB * nc);
+    if (!P || !Unew) { free(P); free(Unew); return OERR_OOM; }
+    /* oracle_fill_guardcells checks nb >= ng; the thick halo may exceed nb, so
+     * fill directly with the per-dimension maps (same rule as the thin fill) */
+    {
+        const long N[3] = {(long)c->nblk[0] * c->nb[0], (long)c->nblk[1] * c->nb[1], (long)c->nblk[2] * c->nb[2]};
+        for (long b = 0; b < NB; b++) {
+            long bx = b % c->nblk[0], by = (b / c->nblk[0]) % c->nblk[1], bz = b / ((long)c->nblk[0] * c->nblk[1]);
+            for (int pk = 0; pk < pn[2]; pk++)
+                for (int pj = 0; pj < pn[1]; pj++)
+                    for (int pi = 0; pi < pn[0]; pi++) {
+                        int fx, fy, fz;
+                        long gx = map_dim(bx * c->nb[0] + pi - g[0], N[0], c->bc[0][0], c->bc[0][1], &fx);
+                        long gy = map_dim(by * c->nb[1] + pj - g[1], N[1], c->bc[1][0], c->bc[1][1], &fy);
+                        long gz = map_dim(bz * c->nb[2] + pk - g[2], N[2], c->bc[2][0], c->bc[2][1], &fz);
+                        long sb = (gx / c->nb[0]) + c->nblk[0] * ((gy / c->nb[1]) + c->nblk[1] * (gz / c->nb[2]));
+                        long sc = ((gz % c->nb[2]) * c->nb[1] + (gy % c->nb[1])) * c->nb[0] + (gx % c->nb[0]);
+                        long pidx = ((long)pk * pn[1] + pj) * pn[0] + pi;
+                        int flip[3] = {fx, fy, fz};
+                        for (int v = 0; v < nv; v++) {
+                            double val = U[(long)v * NB * nc + sb * nc + sc];
+                            if (v >= 1 && v <= ndim && flip[v - 1]) val = -val;
+                            P[(long)v * NB * np + b * np + pidx] = val;
+                        }
+                    }
+        }
+    }
+    int bad = 0;
+#pragma omp parallel reduction(| : bad)
+    {
+        double* T0 = malloc(sizeof(double) * nv * np);  /* U^n on the tile   */
+        double* Tp = malloc(sizeof(double) * nv * np);  /* U^(s-1)           */
+        double* To = malloc(sizeof(double) * nv * np);  /* U^(s)             */
+        double* W = malloc(sizeof(double) * nv * np);   /* primitives of U^(s-1) */
+        double* F[3];
+        for (int d = 0; d < 3; d++) F[d] = malloc(sizeof(double) * nv * np);  /* F[d] at the face below cell */
+#pragma omp for schedule(static)
+        for (long blk = 0; blk < NB; blk++) {
+            for (int v = 0; v < nv; v++)
+                for (long q = 0; q < np; q++) T0[(long)v * np + q] = Tp[(long)v * np + q] = P[(long)v * NB * np + blk * np + q];
+            for (int s = 1; s <= S; s++) {
+                double a, b;
+                oracle_rk_coeffs(S, s, &a, &b);
+                int lo[3], hi[3];  /* cells updated by this stage: [lo, hi) */
+                for (int d = 0; d < 3; d++) {
+                    lo[d] = d < ndim ? s * ngk : 0;
+                    hi[d] = pn[d] - lo[d];
+                }
+                /* primitives of U^(s-1) where valid: distance >= (s-1)*ngk from the edge */
+                for (int k = 0; k < pn[2]; k++)
+                    for (int j = 0; j < pn[1]; j++)
+                        for (int i = 0; i < pn[0]; i++) {
+                            long q = ((long)k * pn[1] + j) * pn[0] + i;
+                            double u[5], w[5];
+                            for (int v = 0; v < nv; v++) u[v] = Tp[(long)v * np + q];
+                            cons_to_prim(ndim, c->gamma, u, w);
+                            for (int v = 0; v < nv; v++) W[(long)v * np + q] = w[v];
+                        }
+                /* face fluxes below each updated cell and below hi (faces lo..hi along d) */
+                for (int d = 0; d < ndim; d++) {
+                    int rot[5], ax[3];
+                    rotation(ndim, d, rot, ax);
+                    int flo[3] = {lo[0], lo[1], lo[2]}, fhi[3] = {hi[0], hi[1], hi[2]};
+                    fhi[d] += 1;
+                    for (int k = flo[2]; k < fhi[2]; k++)
+                        for (int j = flo[1]; j < fhi[1]; j++)
+                            for (int i = flo[0]; i < fhi[0]; i++) {
+                                long right = ((long)k * pn[1] + j) * pn[0] + i;  /* face between right-1 and right */
+                                double st[6 * 5], wl[5], wr[5], fr[5];
+                                for (int m = 0; m < 2 * ngk; m++) {
+                                    long q = right + (long)(m - ngk) * pstride[d];
+                                    for (int v = 0; v < nv; v++) st[m * nv + v] = W[(long)rot[v] * np + q];
+                                }
+                                reconstruct(c->recon, ngk, nv, st, wl, wr);
+                                riemann_ax(c->riemann, nv, c->gamma, ax, wl, wr, fr);
+                                for (int v = 0; v < nv; v++) F[d][(long)rot[v] * np + right] = fr[v];
+                            }
+                }
+                for (int k = lo[2]; k < hi[2]; k++)
+                    for (int j = lo[1]; j < hi[1]; j++)
+                        for (int i = lo[0]; i < hi[0]; i++) {
+                            long q = ((long)k * pn[1] + j) * pn[0] + i;
+                            double unew[5];
+                            for (int v = 0; v < nv; v++) {
+                                double div[3] = {0.0, 0.0, 0.0};
+                                for (int d = 0; d < ndim; d++)
+                                    div[d] = (F[d][(long)v * np + q + pstride[d]] - F[d][(long)v * np + q]) / dx[d];
+                                double L;
+                                if (ndim == 1) L = -(div[0]);
+                                else if (ndim == 2) L = -(div[0] + div[1]);
+                                else L = -(div[0] + div[1]) - div[2];
+                                unew[v] = a * T0[(long)v * np + q] + b * (Tp[(long)v * np + q] + dt * L);
+                                To[(long)v * np + q] = unew[v];
+                            }
+                            double w[5];
+                            cons_to_prim(ndim, c->gamma, unew, w);
+                            int ok = w[0] > 0.0 && w[nv - 1] > 0.0;
+                            for (int v = 0; v < nv; v++) ok = ok && isfinite(unew[v]);
+                            if (!ok) bad = 1;
+                        }
+                for (int v = 0; v < nv; v++)
+                    for (int k = lo[2]; k < hi[2]; k++)
+                        for (int j = lo[1]; j < hi[1]; j++)
+                            for (int i = lo[0]; i < hi[0]; i++) {
+                                long q = ((long)k * pn[1] + j) * pn[0] + i;
+                                Tp[(long)v * np + q] = To[(long)v * np + q];
+                            }
+            }
+            for (int v = 0; v < nv; v++)
+                for (int k = 0; k < c->nb[2]; k++)
+                    for (int j = 0; j < c->nb[1]; j++)
+                        for (int i = 0; i < c->nb[0]; i++) {
+                            long q = ((long)(k + g[2]) * pn[1] + (j + g[1])) * pn[0] + (i + g[0]);
+                            Unew[(long)v * NB * nc + blk * nc + ((long)k * c->nb[1] + j) * c->nb[0] + i] = Tp[(long)v * np + q];
+                        }
+        }
+        free(T0); free(Tp); free(To); free(W);
+        for (int d = 0; d < 3; d++) free(F[d]);
+    }
+    int st = bad ? OERR_NONPHYSICAL : OK;
+    if (st == OK) memcpy(U, Unew, sizeof(double) * nv * NB * nc);
+    free(P);
+    free(Unew);
+    return st;
+}
