@@ -223,6 +223,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c4_sedov3d_plm", choices=sorted(si.PRESETS))
+    ap.add_argument("--telescoping", action="store_true",
+                    help="telescoping SSP-RK steps (NEXT N1; 1-D/2-D, one rank): one launch per step")
     ap.add_argument("--impl", default="spark", choices=["spark", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
@@ -268,9 +270,11 @@ def main():
         if world > 1:
             dist.barrier()
 
+    step = s.step_telescoping if args.telescoping else s.step
+
     # ---- warm-up
     for _ in range(args.warmup):
-        s.step()
+        step()
     stream.synchronize()
 
     # ---- timed region (device time on the library stream)
@@ -281,7 +285,7 @@ def main():
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            s.step()
+            step()
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -296,8 +300,11 @@ def main():
 
     # ---- roofline of the dominant kernel (the fused stage kernel)
     peaks, peak_kind = measured_peaks()
-    bytes_per_step_local = sum(algorithmic_bytes_per_zone(p, st) for st in range(1, p.rk_stages + 1)) * cells_local
-    bytes_per_launch = bytes_per_step_local / p.rk_stages
+    if args.telescoping:  # one launch per step: read U^n, write U^(n+1) (halo re-reads are L2)
+        bytes_per_launch = 2 * p.nvar * 8 * cells_local
+    else:
+        bytes_per_step_local = sum(algorithmic_bytes_per_zone(p, st) for st in range(1, p.rk_stages + 1)) * cells_local
+        bytes_per_launch = bytes_per_step_local / p.rk_stages
     avg_launch_s = stage_ms * 1e-3 / max(stage_launches, 1)
     achieved = bytes_per_launch / avg_launch_s / 1e9
     traffic = ncu_traffic(p.name)
@@ -328,7 +335,7 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             s.set_state(hostU.numpy())
-            s.step()
+            step()
             s.get_state(out=hostU.numpy())
         torch.cuda.synchronize()
         barrier()
@@ -348,7 +355,7 @@ def main():
         t0 = time.perf_counter()
         s.set_state(hostU.numpy())
         for _ in range(args.steps):
-            s.step(sync=True)
+            step(sync=True)
         s.get_state(out=hostU.numpy())
         torch.cuda.synchronize()
         barrier()
@@ -397,7 +404,8 @@ def main():
             "config": {"workload": p.name, "cells": p.ncells, "cells_per_gpu": cells_local,
                        "block": list(p.nb), "blocks": list(p.nblk), "recon": ["first", "plm", "weno5"][p.recon],
                        "riemann": ["hll", "hllc"][p.riemann], "rk_stages": p.rk_stages, "ng": p.ng,
-                       "parallelism": f"blocks over {world} GPU(s)", "l2": "state per copy > L2 (no flush needed)"},
+                       "parallelism": f"blocks over {world} GPU(s)", "l2": "state per copy > L2 (no flush needed)",
+                       "rk_mode": "telescoping" if args.telescoping else "non-telescoping"},
             "roofline": roofline, "roofline_fp64": roofline_fp64, "hbm_calibration_gbs": calib,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": total_launches,

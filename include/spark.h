@@ -195,6 +195,16 @@ spark_status spark_fill_guardcells(spark_ctx* ctx, double* padded_out);
  * is rolled back to U^n of this step. */
 spark_status spark_step(spark_ctx* ctx, double dt, double t_end, double* dt_used);
 
+/* Telescoping SSP-RK step (lst:spark-telescoping
+ * P:1598-1604): one guard gather per STEP with S*NGK layers
+ * (NGK = reconstruction half-width), then all S stages per block with the halo
+ * area updated too, in ONE kernel (the intermediate stages stay on chip).
+ * Guards beyond a physical boundary are filled once and evolved (DESIGN.md
+ * reading R17); with periodic boundaries the result equals spark_step.
+ * Single-rank contexts, ndim <= 2 (a 3-D tile does not fit on chip); same dt
+ * and dt_used semantics as spark_step. */
+spark_status spark_step_telescoping(spark_ctx* ctx, double dt, double t_end, double* dt_used);
+
 /* Enqueue up to max_steps steps (CFL dt, clipped to t_end), synchronising
  * every check_every steps (<= 0: only at the end) to stop once t_end is
  * reached.  *steps_done receives the number of steps that advanced time. */

@@ -886,3 +886,56 @@ extern "C" spark_status spark_axpy(int32_t device, int32_t variant, int64_t n, d
         CU(spark::launch_axpy(variant, n, a, x, y, sms, static_cast<cudaStream_t>(cuda_stream)));
     });
 }
+
+extern "C" spark_status spark_step_telescoping(spark_ctx* ctx, double dt, double t_end, double* dt_used) {
+    if (!ctx) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        if (!ctx->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
+        if (ctx->nranks != 1 || ctx->comm || ctx->group)
+            throw Error(SPARK_ERR_STATE, "telescoping steps need a single-rank context");
+        if (ctx->cfg.ndim > 2) throw Error(SPARK_ERR_ARG, "telescoping steps support ndim <= 2");
+        const int S = ctx->cfg.rk_stages;
+        const int ngk = stencil_ng(ctx->cfg.recon);
+        for (int d = 0; d < ctx->cfg.ndim; d++)
+            if (S * ngk > (long long)ctx->cfg.nb[d] * ctx->cfg.nblk[d])
+                throw Error(SPARK_ERR_ARG, "telescoped halo deeper than the domain");
+        if (spark::telescope_smem_bytes(ctx->plan.geo, ctx->cfg.recon, S) > 227 * 1024)
+            throw Error(SPARK_ERR_ARG, "telescoping tile exceeds shared memory (block too large)");
+        set_device(ctx);
+        const int old_n = ctx->n_idx;
+        launched(ctx, spark::launch_step_begin(ctx->sc, dt, t_end, ctx->cfg.cfl, ctx->stream), "step begin");
+        const int out = (ctx->n_idx + 1) % 3;
+        spark::StageArgs A{};
+        A.g = ctx->plan.geo;
+        A.uprev = ctx->U[ctx->n_idx];
+        A.un = ctx->U[ctx->n_idx];
+        A.uout = ctx->U[out];
+        A.sc = ctx->sc;
+        A.dt_ptr = &ctx->sc->dt;
+        A.last = 1;
+        A.honor_active = 1;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (ctx->prof) {
+            if (ctx->ev_used == ctx->ev.size()) {
+                cudaEvent_t x, y;
+                CU(cudaEventCreate(&x));
+                CU(cudaEventCreate(&y));
+                ctx->ev.emplace_back(x, y);
+            }
+            e0 = ctx->ev[ctx->ev_used].first;
+            e1 = ctx->ev[ctx->ev_used].second;
+            ctx->ev_used++;
+            CU(cudaEventRecord(e0, ctx->stream));
+        }
+        launched(ctx, spark::launch_telescope(A, ctx->cfg.recon, ctx->cfg.riemann, S, ctx->stream), "telescope");
+        ctx->stage_launches++;
+        if (ctx->prof) CU(cudaEventRecord(e1, ctx->stream));
+        ctx->n_idx = out;
+        if (dt_used) {
+            sync_and_check(ctx, true, old_n);
+            double h;
+            CU(cudaMemcpy(&h, &ctx->sc->dt, sizeof(double), cudaMemcpyDeviceToHost));
+            *dt_used = h;
+        }
+    });
+}

@@ -75,6 +75,8 @@ cudaError_t launch_selftest_riemann(int riemann, int ndim, int dir, double gamma
                                     const double* wr, double* f);
 cudaError_t launch_axpy(int variant, int64_t n, double a, const double* x, double* y, int sms, cudaStream_t s);
 size_t stage_smem_bytes(const Geo& g, int recon);
+size_t telescope_smem_bytes(const Geo& g, int recon, int S);
+cudaError_t launch_telescope(const StageArgs& a, int recon, int riemann, int S, cudaStream_t s);
 int stage_block_threads(const Geo& g, int recon);
 
 }  // namespace spark
