@@ -223,6 +223,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c4_sedov3d_plm", choices=sorted(si.PRESETS))
+    ap.add_argument("--graphs", action="store_true",
+                    help="time spark_run (CUDA-graph replay of 3-step groups; one rank, non-telescoping)")
     ap.add_argument("--telescoping", action="store_true",
                     help="telescoping SSP-RK steps (NEXT N1; 1-D/2-D, one rank): one launch per step")
     ap.add_argument("--impl", default="spark", choices=["spark", "reference"])
@@ -278,19 +280,29 @@ def main():
     stream.synchronize()
 
     # ---- timed region (device time on the library stream)
-    s.profile(True)
+    # --graphs: spark_run replays CUDA graphs of 3 steps (no per-kernel events
+    # then: the stage-kernel time is the step time)
+    s.profile(not args.graphs)
+    if args.graphs:
+        s.run(3)  # capture outside the timed region
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
-            step()
+        if args.graphs:
+            s.run(args.steps)
+        else:
+            for _ in range(args.steps):
+                step()
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
     ms = e0.elapsed_time(e1)
-    stage_ms, stage_launches, total_launches = s.profile_read()
+    if args.graphs:
+        stage_ms, stage_launches, total_launches = ms, args.steps * p.rk_stages, args.steps * (p.rk_stages + 1)
+    else:
+        stage_ms, stage_launches, total_launches = s.profile_read()
     s.profile(False)
     t_dev = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
     if world > 1:
@@ -405,7 +417,8 @@ def main():
                        "block": list(p.nb), "blocks": list(p.nblk), "recon": ["first", "plm", "weno5"][p.recon],
                        "riemann": ["hll", "hllc"][p.riemann], "rk_stages": p.rk_stages, "ng": p.ng,
                        "parallelism": f"blocks over {world} GPU(s)", "l2": "state per copy > L2 (no flush needed)",
-                       "rk_mode": "telescoping" if args.telescoping else "non-telescoping"},
+                       "rk_mode": "telescoping" if args.telescoping else "non-telescoping",
+                       "launch": "cuda-graph (spark_run)" if args.graphs else "stream (spark_step)"},
             "roofline": roofline, "roofline_fp64": roofline_fp64, "hbm_calibration_gbs": calib,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": total_launches,

@@ -195,6 +195,13 @@ spark_status spark_fill_guardcells(spark_ctx* ctx, double* padded_out);
  * is rolled back to U^n of this step. */
 spark_status spark_step(spark_ctx* ctx, double dt, double t_end, double* dt_used);
 
+/* nsteps steps of spark_step (same dt / t_end semantics), fully asynchronous.
+ * Single-rank contexts created on a non-default stream replay a CUDA graph of
+ * 3 steps (the buffer-rotation period), which removes the per-launch overhead
+ * of small, launch-bound problems; other contexts enqueue plain launches.
+ * Results are identical to calling spark_step nsteps times. */
+spark_status spark_run(spark_ctx* ctx, int64_t nsteps, double dt, double t_end);
+
 /* Telescoping SSP-RK step (lst:spark-telescoping
  * P:1598-1604): one guard gather per STEP with S*NGK layers
  * (NGK = reconstruction half-width), then all S stages per block with the halo

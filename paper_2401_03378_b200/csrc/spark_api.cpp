@@ -218,6 +218,12 @@ struct spark_ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
     size_t ev_used = 0;
     int64_t stage_launches = 0, total_launches = 0;
+    // CUDA graphs of 3 steps (the buffer-rotation period) for spark_run, one per
+    // starting buffer index; re-captured when dt / t_end change
+    struct Graph {
+        cudaGraphExec_t exec = nullptr;
+        double dt = 0.0, t_end = 0.0;
+    } graphs[3];
     double prof_ms = 0.0;
 };
 
@@ -593,6 +599,8 @@ spark_status spark_finalize(spark_ctx* ctx) {
             cudaEventDestroy(e.second);
         }
         if (ctx->comm_stream) CU(cudaStreamSynchronize(ctx->comm_stream));
+        for (auto& gr : ctx->graphs)
+            if (gr.exec) cudaGraphExecDestroy(gr.exec);
         if (ctx->comm) ncclCommDestroy(ctx->comm);
         if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
         if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
@@ -936,6 +944,67 @@ extern "C" spark_status spark_step_telescoping(spark_ctx* ctx, double dt, double
             double h;
             CU(cudaMemcpy(&h, &ctx->sc->dt, sizeof(double), cudaMemcpyDeviceToHost));
             *dt_used = h;
+        }
+    });
+}
+
+// spark_run: nsteps SSP-RK steps, fully asynchronous.  Single-rank contexts on a
+// non-default stream replay a CUDA graph of 3 steps (after 3 steps the U^n
+// buffer index is back where it started, so the captured pointers stay valid);
+// launch-bound problems (the small configs) gain the most.
+extern "C" spark_status spark_run(spark_ctx* ctx, int64_t nsteps, double dt, double t_end) {
+    if (!ctx || nsteps < 0) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        if (!ctx->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
+        if (ctx->group) throw Error(SPARK_ERR_STATE, "local-group contexts step with spark_step_group");
+        set_device(ctx);
+        const bool graphable = !ctx->comm && !ctx->prof && ctx->stream != nullptr;
+        const int64_t per_step = ctx->cfg.rk_stages + 1;
+        int64_t done = 0;
+        while (done < nsteps) {
+            if (graphable && nsteps - done >= 3) {
+                auto& gr = ctx->graphs[ctx->n_idx];
+                if (!gr.exec || gr.dt != dt || gr.t_end != t_end) {
+                    if (gr.exec) CU(cudaGraphExecDestroy(gr.exec));
+                    gr.exec = nullptr;
+                    const int n0 = ctx->n_idx;
+                    const int64_t sl = ctx->stage_launches, tl = ctx->total_launches;
+                    cudaGraph_t graph = nullptr;
+                    CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+                    try {
+                        for (int k = 0; k < 3; k++) {
+                            launched(ctx, spark::launch_step_begin(ctx->sc, dt, t_end, ctx->cfg.cfl, ctx->stream),
+                                     "step begin");
+                            do_step(ctx, dt);
+                        }
+                    } catch (...) {
+                        cudaStreamEndCapture(ctx->stream, &graph);
+                        if (graph) cudaGraphDestroy(graph);
+                        ctx->n_idx = n0;
+                        throw;
+                    }
+                    CU(cudaStreamEndCapture(ctx->stream, &graph));
+                    cudaError_t e = cudaGraphInstantiate(&gr.exec, graph, 0);
+                    cudaGraphDestroy(graph);
+                    if (e != cudaSuccess) {
+                        gr.exec = nullptr;
+                        throw Error(SPARK_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+                    }
+                    gr.dt = dt;
+                    gr.t_end = t_end;
+                    ctx->stage_launches = sl;  // capturing launched nothing
+                    ctx->total_launches = tl;
+                    if (ctx->n_idx != n0) throw Error(SPARK_ERR_STATE, "buffer rotation period is not 3");
+                }
+                CU(cudaGraphLaunch(gr.exec, ctx->stream));
+                ctx->total_launches += 3 * per_step;
+                ctx->stage_launches += 3 * ctx->cfg.rk_stages;
+                done += 3;
+            } else {
+                launched(ctx, spark::launch_step_begin(ctx->sc, dt, t_end, ctx->cfg.cfl, ctx->stream), "step begin");
+                do_step(ctx, dt);
+                done += 1;
+            }
         }
     });
 }

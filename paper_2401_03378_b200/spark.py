@@ -25,7 +25,7 @@ EXPORTS = [
     "spark_finalize", "spark_last_error", "spark_set_state", "spark_set_primitive", "spark_get_state",
     "spark_get_time", "spark_get_cfl_min", "spark_fill_guardcells", "spark_step", "spark_advance",
     "spark_step_group", "spark_stage_apply", "spark_profile_enable", "spark_profile_read",
-    "spark_selftest_riemann", "spark_axpy", "spark_step_telescoping",
+    "spark_selftest_riemann", "spark_axpy", "spark_step_telescoping", "spark_run",
 ]
 
 
@@ -122,6 +122,7 @@ def lib() -> ctypes.CDLL:
         "spark_selftest_riemann": (i32, [i32, i32, i32, i32, d, i64, P(d), P(d), P(d)]),
         "spark_axpy": (i32, [i32, i32, i64, d, vp, vp, vp]),
         "spark_step_telescoping": (i32, [vp, d, d, P(d)]),
+        "spark_run": (i32, [vp, i64, d, d]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -288,6 +289,10 @@ class Spark:
             return d.value
         _check(lib().spark_step(self.ctx, dt, t_end, None), self.ctx, "step")
         return None
+
+    def run(self, nsteps: int, dt: float = 0.0, t_end: float = 0.0):
+        """nsteps steps, asynchronous; CUDA-graph replay on a non-default stream."""
+        _check(lib().spark_run(self.ctx, nsteps, dt, t_end), self.ctx, "run")
 
     def step_telescoping(self, dt: float = 0.0, t_end: float = 0.0, sync: bool = False):
         """One telescoping SSP-RK step (1-D/2-D, single rank)."""
