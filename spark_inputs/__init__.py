@@ -202,6 +202,56 @@ def _sedov_ndep(p: Problem, r0: float) -> int:
     return int((r2 < r0 * r0).sum())
 
 
+def sedov_deposit(p: Problem, e_blast: float = 1.0, p_amb: float = 1e-5, r0_cells: float = 3.5):
+    """The Sedov IC in sparse form: (global (x, y, z) cell indices of the deposit,
+    p_dep, p_amb).  Same membership test and p_dep expression as ``sedov``, so
+    ``sedov_device`` is bit-identical to ``sedov`` (tests/test_inputs.py)."""
+    n = [p.nblk[d] * p.nb[d] for d in range(3)]
+    dxs = [(p.hi[d] - p.lo[d]) / n[d] for d in range(3)]
+    r0 = r0_cells * dxs[0]
+    k = int(np.ceil(r0 / dxs[0])) + 2
+    lo = [max(0, n[d] // 2 - k) if d < p.ndim else 0 for d in range(3)]
+    hi = [min(n[d], n[d] // 2 + k) if d < p.ndim else 1 for d in range(3)]
+    x, y, z = centres(p, (tuple(lo), tuple(hi[d] - lo[d] for d in range(3))))
+    c = [0.5 * (p.lo[d] + p.hi[d]) for d in range(3)]
+    r2 = (x - c[0]) ** 2
+    if p.ndim >= 2:
+        r2 = r2 + (y - c[1]) ** 2
+    if p.ndim >= 3:
+        r2 = r2 + (z - c[2]) ** 2
+    kz, jy, ix = np.nonzero(r2 < r0 * r0)
+    cells = np.stack([ix + lo[0], jy + lo[1], kz + lo[2]], axis=1)
+    dV = float(np.prod(dxs[: p.ndim]))
+    p_dep = (p.gamma - 1.0) * e_blast / (len(cells) * dV)
+    return cells, p_dep, p_amb
+
+
+def sedov_device(p: Problem, box=None, device="cuda"):
+    """``sedov(p, box)`` built directly in device memory (torch), canonical block
+    layout of the sub-box: a fill plus a scatter of the ~200 deposit cells.  For
+    grids whose host copy would not fit (configs[4]: 1024^3 x 5 x 8 B = 40 GiB)."""
+    import torch
+
+    n = [p.nblk[d] * p.nb[d] for d in range(3)]
+    lo_c, n_c = box if box is not None else ((0, 0, 0), tuple(n))
+    nbk = [n_c[d] // p.nb[d] for d in range(3)]
+    nblocks = nbk[0] * nbk[1] * nbk[2]
+    W = torch.zeros((p.nvar, nblocks, p.nb[2], p.nb[1], p.nb[0]), dtype=torch.float64, device=device)
+    cells, p_dep, p_amb = sedov_deposit(p)
+    W[0].fill_(1.0)
+    W[p.ndim + 1].fill_(p_amb)
+    loc = cells - np.asarray(lo_c)[None, :]
+    inside = np.all((loc >= 0) & (loc < np.asarray(n_c)[None, :]), axis=1)
+    loc = loc[inside]
+    if len(loc):
+        nb = np.asarray(p.nb)
+        bq, r = loc // nb, loc % nb
+        b = bq[:, 0] + nbk[0] * (bq[:, 1] + nbk[1] * bq[:, 2])
+        idx = ((b * p.nb[2] + r[:, 2]) * p.nb[1] + r[:, 1]) * p.nb[0] + r[:, 0]
+        W[p.ndim + 1].view(-1)[torch.from_numpy(idx).to(W.device)] = p_dep
+    return W
+
+
 def random_state(p: Problem, seed: int, blocky: bool = False) -> np.ndarray:
     """rho, p ~ U[0.5,1.5]; u_d ~ U[-0.5,0.5]; 'blocky' adds x-jumps (rho x10, p x100)."""
     g = np.random.Generator(np.random.PCG64(seed))
