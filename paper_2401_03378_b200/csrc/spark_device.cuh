@@ -81,21 +81,27 @@ __host__ __device__ __forceinline__ long long dbits(double x) {
 
 __host__ __device__ __forceinline__ bool positive(double x) { return dbits(x) > 0; }
 
-// minmod(a, b): 0 unless a and b are both nonzero with the same sign, else the
-// one of smaller magnitude (ties: b).  Integer pipe only; bitwise equal to
-// the oracle's comparison form (reading R2).
-__host__ __device__ __forceinline__ double minmod(double a, double b) {
-    // m = min(|a|, |b|) carries the sign of a (= sign of b when kept); a zero
-    // m gives a signed zero, which W +- d/2 turns into W exactly, as +0 does.
-    const double m = fmin(fabs(a), fabs(b));
+__host__ __device__ __forceinline__ double dfrombits(long long b) {
 #ifdef __CUDA_ARCH__
-    const int ha = __double2hiint(a), hb = __double2hiint(b);
-    const double r = __hiloint2double(__double2hiint(m) | (ha & 0x80000000), __double2loint(m));
-    return (ha ^ hb) >= 0 ? r : 0.0;
+    return __longlong_as_double(b);
 #else
-    const long long ia = dbits(a), ib = dbits(b);
-    return (ia ^ ib) >= 0 ? copysign(m, a) : 0.0;
+    double x;
+    __builtin_memcpy(&x, &b, 8);
+    return x;
 #endif
+}
+
+// minmod(a, b): 0 unless a and b are both nonzero with the same sign, else the
+// one of smaller magnitude (ties: b).  Integer pipe only (no DSETP / fmin NaN
+// handling): magnitudes compare as unsigned bit patterns.  Bitwise equal to
+// the oracle's comparison form (reading R2); a kept zero is signed,
+// which W +- d/2 turns into W exactly, as +0 does.
+__host__ __device__ __forceinline__ double minmod(double a, double b) {
+    const long long ia = dbits(a), ib = dbits(b);
+    const unsigned long long ma = (unsigned long long)ia & 0x7fffffffffffffffull;
+    const unsigned long long mb = (unsigned long long)ib & 0x7fffffffffffffffull;
+    const long long r = ma < mb ? ia : ib;
+    return (ia ^ ib) >= 0 ? dfrombits(r) : 0.0;
 }
 
 // ------------------------------------------------------------------- EOS
@@ -186,8 +192,11 @@ __host__ __device__ __forceinline__ void riemann(const double* wl, const double*
     // c = sqrt(gamma p / rho) = gamma p / sqrt(gamma p rho): no reciprocal of rho needed
     const double gpl = gamma * pl, gpr = gamma * pr;
     const double cl = gpl * rsqrt_fast(gpl * rl), cr = gpr * rsqrt_fast(gpr * rr);
-    const double sl = fmin(ul - cl, ur - cr);
-    const double sr = fmax(ul + cl, ur + cr);
+    // Davis estimates; plain compares instead of fmin/fmax (identical for
+    // non-NaN operands) avoid the NaN fix-up instructions
+    const double al = ul - cl, ar = ur - cr, bl = ul + cl, br = ur + cr;
+    const double sl = al < ar ? al : ar;
+    const double sr = bl > br ? bl : br;
     if (RS == 1) {
         const double ql = rl * (sl - ul), qr = rr * (sr - ur);  // rho_K (S_K - u_K)
         const double sstar = (pr - pl + ul * ql - ur * qr) * rcp(ql - qr);

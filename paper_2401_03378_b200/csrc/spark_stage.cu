@@ -99,6 +99,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     double* YA = XB + NV * fxn;                // [NV][fyn]
     double* YB = YA + NV * fyn;                // [NV][fyn]
     double* stg = YB + NV * fyn;               // [2][NV][P] staged S4 operands (STAGE_OPS)
+#ifdef ABL_NOHALO
+    for (int q = threadIdx.x; q < NV * CP; q += blockDim.x) cur[q] = 1.0;
+    __syncthreads();
+#endif
 
     const double dt = A.dt_ptr ? *A.dt_ptr : A.dt_value;
     const double a = A.a, bco = A.b;
@@ -222,13 +226,39 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     // 16x16 planes: nh <= 256, so thread h owns halo cell h for every plane and
     // prefetches it one plane ahead (raw conserved values in registers)
     constexpr bool HPF = NBX == 16 && NBY == 16;
+#ifdef ABL_NOHALO
+    const bool hact = false;
+#else
     const bool hact = HPF && tid < nh;
+#endif
     int hcx = 0, hcy = 0;
     double hpre[NV];
+    // Per-plane sources resolved once: a halo cell in a face-neighbour block of
+    // this sub-box is a plain column (stride P per plane) of that block; others
+    // (physical boundary / received slab) take the general gather every plane.
+    const double* hsrc = nullptr;
     if (hact) {
         halo_cell(tid, hcx, hcy);
+        int q0 = bx, q1 = by, lx = hcx, ly = hcy;
+        if (hcx < 0 || hcx >= nb0) { q0 += hcx < 0 ? -1 : 1; lx = hcx < 0 ? hcx + nb0 : hcx - nb0; }
+        else { q1 += hcy < 0 ? -1 : 1; ly = hcy < 0 ? hcy + nb1 : hcy - nb1; }
+        if (q0 >= 0 && q0 < g.bn[0] && q1 >= 0 && q1 < g.bn[1])
+            hsrc = up + (q0 + (long long)g.bn[0] * (q1 + (long long)g.bn[1] * bz)) * cpb + (long long)ly * nb0 + lx;
         load_cons(hcx, hcy, 0, hpre);
     }
+    auto load_halo = [&](int z, double* u) {
+        if (hsrc) ldg_cons<NV>(hsrc + (long long)z * P, ncell, u);
+        else load_cons(hcx, hcy, z, u);
+    };
+    // this column: planes z < nb2 of the own block, z >= nb2 of the block above
+    // (if inside the sub-box, else the general gather)
+    const double* csrc = up + bbase + (long long)tj * nb0 + ti;
+    const double* casrc = (NDIM == 3 && bz + 1 < g.bn[2]) ? csrc + (long long)g.bn[0] * g.bn[1] * cpb : nullptr;
+    auto load_col = [&](int z, double* u) {
+        if (z < nb2) ldg_cons<NV>(csrc + (long long)z * P, ncell, u);
+        else if (casrc) ldg_cons<NV>(casrc + (long long)(z - nb2) * P, ncell, u);
+        else load_cons(ti, tj, z, u);
+    };
 
     // raw conserved values of this column's plane kk+NG, loaded one plane ahead
     double pre[NV];
@@ -243,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             double w[NV];
             if (NDIM == 3) {
                 ok &= cons_to_prim<NV>(pre, w, gm1);
-                if (kk + 1 < nb2) load_cons(ti, tj, kk + 1 + NG, pre);  // prefetch the next plane
+                if (kk + 1 < nb2) load_col(kk + 1 + NG, pre);  // prefetch the next plane
 #pragma unroll
                 for (int v = 0; v < NV; v++) ring_at(kk + NG, v) = w[v];
 #pragma unroll
@@ -258,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             if (hact) {
                 double w[NV];
                 ok &= cons_to_prim<NV>(hpre, w, gm1);
-                if (kk + 1 < nb2) load_cons(hcx, hcy, kk + 1, hpre);
+                if (kk + 1 < nb2) load_halo(kk + 1, hpre);
 #pragma unroll
                 for (int v = 0; v < NV; v++) cur[v * CP + (hcy + RO) * cw + hcx + NG] = w[v];
             }
@@ -316,6 +346,9 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
         }
         // edge states from the halo cells: one (cell, variable) item per thread
         // round so the extra work spreads over all warps
+#ifdef ABL_NOEDGE
+        if (false)
+#endif
         for (int qv = tid; qv < nbr * NV; qv += blockDim.x) {
             const int v = qv / nbr, q = qv - v * nbr;
             const bool xd = q < 2 * nb1;
@@ -431,7 +464,11 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                     }
                 }
             }
+#ifdef ABL_NOBND
+            if (false) {
+#else
             if (tid < 32) {  // warp 0: boundary face (+ its z faces)
+#endif
                 const bool isy = tid >= 16;
                 const int q = tid & 15;
                 double bl[NV], br[NV], fb[NV];

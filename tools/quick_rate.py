@@ -7,6 +7,9 @@ sys.path.insert(0, ".")
 import spark_inputs as si  # noqa: E402
 from paper_2401_03378_b200 import spark  # noqa: E402
 
+if len(sys.argv) > 1 and sys.argv[1].endswith(".so"):  # a variant library (tools/ablate.sh)
+    spark.LIB_PATH = sys.argv.pop(1)
+
 p = si.PRESETS[sys.argv[1]]
 kw = {}
 for a in sys.argv[2:]:
