@@ -174,6 +174,9 @@ Plan make_plan(const spark_config* c, int rank, int nranks, bool self_exchange =
             if (e != d) s *= g.cn[e];
         g.slab[d] = d < c->ndim ? s : 0;
     }
+    // kernels keep variable strides (ncell, slab sizes) in 32-bit registers; a
+    // sub-box this large would need > 250 GB of state anyway
+    if (g.ncell >= (1LL << 31)) throw Error(SPARK_ERR_ARG, "sub-box exceeds 2^31 cells (split over more ranks)");
     g.gamma = c->gamma;
     g.cfl = c->cfl;
     return p;

@@ -278,12 +278,16 @@ __host__ __device__ __forceinline__ void riemann(const double* wl, const double*
 // the normal momentum negated).  Returns false (out unset) when the cell lies
 // outside the sub-box in two or more peer directions (an edge or corner owned
 // by a diagonal rank; never needed by the star stencil).
-template <int NV>
-__device__ __forceinline__ bool fetch_cons(const Geo& g, const double* __restrict__ u,
-                                           const double* const (&halo)[3][2], int l0, int l1, int l2,
-                                           double* out) {
+struct Src {
+    const double* p;  // variable 0 of the source cell
+    long long vs;     // stride between variables
+    int flip;         // bit 1+d: negate momentum d (reflecting boundary)
+};
+
+__device__ __forceinline__ bool fetch_src(const Geo& g, const double* __restrict__ u,
+                                          const double* const (&halo)[3][2], int l0, int l1, int l2, Src& src) {
     int l[3] = {l0, l1, l2};
-    bool flip[3] = {false, false, false};
+    int flip = 0;
     int hd = -1, hs = 0;
 #pragma unroll
     for (int d = 0; d < 3; d++) {
@@ -306,35 +310,51 @@ __device__ __forceinline__ bool fetch_cons(const Geo& g, const double* __restric
                     gx = side ? N - 1 : 0;
                 } else {
                     gx = side ? 2 * N - 1 - gx : -1 - gx;
-                    flip[d] = true;
+                    flip |= 2 << d;
                 }
                 l[d] = gx - g.off[d];
             }
         }
     }
-    const double* base;
-    long long idx, stride;
+    long long idx;
     if (hd >= 0) {
         int c[3] = {l[0], l[1], l[2]};
         c[hd] = hs ? l[hd] - g.cn[hd] : l[hd] + g.ng;
         const int e0 = hd == 0 ? g.ng : g.cn[0];
         const int e1 = hd == 1 ? g.ng : g.cn[1];
         idx = ((long long)c[2] * e1 + c[1]) * e0 + c[0];
-        base = halo[hd][hs];
-        stride = g.slab[hd];
+        src.p = halo[hd][hs] + idx;
+        src.vs = g.slab[hd];
     } else {
         const int bx = l[0] / g.nb[0], by = l[1] / g.nb[1], bz = l[2] / g.nb[2];
         const long long blk = bx + (long long)g.bn[0] * (by + (long long)g.bn[1] * bz);
         idx = blk * g.cpb + ((long long)(l[2] - bz * g.nb[2]) * g.nb[1] + (l[1] - by * g.nb[1])) * g.nb[0] +
               (l[0] - bx * g.nb[0]);
-        base = u;
-        stride = g.ncell;
+        src.p = u + idx;
+        src.vs = g.ncell;
     }
+    src.flip = flip;
+    return true;
+}
+
+// conserved values at a source, reflect flips applied (sign-bit xor)
+template <int NV>
+__device__ __forceinline__ void load_src(const double* p, long long vs, int flip, double* out) {
 #pragma unroll
-    for (int v = 0; v < NV; v++) out[v] = base[v * stride + idx];
+    for (int v = 0; v < NV; v++) out[v] = __ldg(p + v * vs);
 #pragma unroll
     for (int d = 0; d < NV - 2; d++)
-        if (flip[d]) out[1 + d] = -out[1 + d];
+        out[1 + d] = __hiloint2double(__double2hiint(out[1 + d]) ^ (((flip >> (1 + d)) & 1) << 31),
+                                      __double2loint(out[1 + d]));
+}
+
+template <int NV>
+__device__ __forceinline__ bool fetch_cons(const Geo& g, const double* __restrict__ u,
+                                           const double* const (&halo)[3][2], int l0, int l1, int l2,
+                                           double* out) {
+    Src s;
+    if (!fetch_src(g, u, halo, l0, l1, l2, s)) return false;
+    load_src<NV>(s.p, s.vs, s.flip, out);
     return true;
 }
 

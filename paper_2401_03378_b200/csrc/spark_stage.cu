@@ -236,20 +236,23 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     // Per-plane sources resolved once: a halo cell in a face-neighbour block of
     // this sub-box is a plain column (stride P per plane) of that block; others
     // (physical boundary / received slab) take the general gather every plane.
-    const double* hsrc = nullptr;
+    // The source of halo cell (x, y) in plane z (face-neighbour block, received
+    // slab, or physical-boundary image) is affine in z: resolved once (two
+    // fetch_src calls), the z-march does plain strided loads.  Compact form:
+    // base pointer, 32-bit variable stride, and plane stride << 4 | flip bits.
+    const double* hp = up;
+    int hvs = 0, hzf = 0;
     if (hact) {
         halo_cell(tid, hcx, hcy);
-        int q0 = bx, q1 = by, lx = hcx, ly = hcy;
-        if (hcx < 0 || hcx >= nb0) { q0 += hcx < 0 ? -1 : 1; lx = hcx < 0 ? hcx + nb0 : hcx - nb0; }
-        else { q1 += hcy < 0 ? -1 : 1; ly = hcy < 0 ? hcy + nb1 : hcy - nb1; }
-        if (q0 >= 0 && q0 < g.bn[0] && q1 >= 0 && q1 < g.bn[1])
-            hsrc = up + (q0 + (long long)g.bn[0] * (q1 + (long long)g.bn[1] * bz)) * cpb + (long long)ly * nb0 + lx;
-        load_cons(hcx, hcy, 0, hpre);
+        Src s0, s1;
+        fetch_src(g, up, A.halo, cx0 + hcx, cy0 + hcy, cz0, s0);
+        fetch_src(g, up, A.halo, cx0 + hcx, cy0 + hcy, cz0 + (nb2 > 1 ? 1 : 0), s1);
+        hp = s0.p;
+        hvs = (int)s0.vs;
+        hzf = (int)((s1.p - s0.p) * 16) | s0.flip;
+        load_src<NV>(hp, hvs, s0.flip, hpre);
     }
-    auto load_halo = [&](int z, double* u) {
-        if (hsrc) ldg_cons<NV>(hsrc + (long long)z * P, ncell, u);
-        else load_cons(hcx, hcy, z, u);
-    };
+    auto load_halo = [&](int z, double* u) { load_src<NV>(hp + (long long)z * (hzf >> 4), hvs, hzf & 15, u); };
     // this column: planes z < nb2 of the own block, z >= nb2 of the block above
     // (if inside the sub-box, else the general gather)
     const double* csrc = up + bbase + (long long)tj * nb0 + ti;

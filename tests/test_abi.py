@@ -117,6 +117,18 @@ def test_required_bytes_scale():
     assert b8 < b1 / 7
 
 
+def test_sub_box_cell_limit():
+    """configs[4] (1024^3) fits one rank; 2048^3 needs >= 4 ranks (2^31 cells per sub-box)."""
+    c5 = si.PRESETS["c5_sedov3d_plm"]
+    assert spark.required_bytes(c5.config(), 0, 1) >= 3 * 5 * 1024 ** 3 * 8
+    big = c5.with_(nblk=(128, 128, 128)).config()
+    with pytest.raises(spark.SparkError):
+        spark.required_bytes(big, 0, 1)
+    with pytest.raises(spark.SparkError):
+        spark.required_bytes(big, 0, 2)
+    spark.required_bytes(big, 0, 8)
+
+
 def test_product_path_does_not_touch_oracle():
     """The binding and the CUDA sources never import, link or name the oracle."""
     pkg = os.path.join(ROOT, "paper_2401_03378_b200")
