@@ -244,13 +244,17 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     int hvs = 0, hzf = 0;
     if (hact) {
         halo_cell(tid, hcx, hcy);
-        Src s0, s1;
-        fetch_src(g, up, A.halo, cx0 + hcx, cy0 + hcy, cz0, s0);
-        fetch_src(g, up, A.halo, cx0 + hcx, cy0 + hcy, cz0 + (nb2 > 1 ? 1 : 0), s1);
-        hp = s0.p;
-        hvs = (int)s0.vs;
-        hzf = (int)((s1.p - s0.p) * 16) | s0.flip;
-        load_src<NV>(hp, hvs, s0.flip, hpre);
+        if (NDIM == 3) {
+            Src s0, s1;
+            fetch_src(g, up, A.halo, cx0 + hcx, cy0 + hcy, cz0, s0);
+            fetch_src(g, up, A.halo, cx0 + hcx, cy0 + hcy, cz0 + (nb2 > 1 ? 1 : 0), s1);
+            hp = s0.p;
+            hvs = (int)s0.vs;
+            hzf = (int)((s1.p - s0.p) * 16) | s0.flip;
+            load_src<NV>(hp, hvs, s0.flip, hpre);
+        } else {  // one plane: a single load through the block-neighbour fast path
+            load_cons(hcx, hcy, 0, hpre);
+        }
     }
     auto load_halo = [&](int z, double* u) { load_src<NV>(hp + (long long)z * (hzf >> 4), hvs, hzf & 15, u); };
     // this column: planes z < nb2 of the own block, z >= nb2 of the block above
