@@ -59,6 +59,7 @@ class _Cfg(ctypes.Structure):
         ("rk_stages", ctypes.c_int32),
         ("gamma", ctypes.c_double),
         ("cfl", ctypes.c_double),
+        ("grav", ctypes.c_double * 3),
     ]
 
 
@@ -80,6 +81,9 @@ def lib():
             "oracle_plm_face": (None, [d, d, d, d, dp, dp]),
             "oracle_weno5_edge": (d, [d, d, d, d, d]),
             "oracle_weno5_face": (None, [dp, dp, dp]),
+            "oracle_mc_face": (None, [d, d, d, d, dp, dp]),
+            "oracle_weno5z_edge": (d, [d, d, d, d, d]),
+            "oracle_weno5z_face": (None, [dp, dp, dp]),
             "oracle_riemann": (None, [i32, i32, d, dp, dp, dp]),
             "oracle_dt_raw": (d, [P(_Cfg), dp]),
             "oracle_dt": (d, [P(_Cfg), dp, d, d]),
@@ -114,6 +118,7 @@ class Config:
     rk_stages: int = 2
     gamma: float = 1.4
     cfl: float = 0.8
+    grav: tuple = (0.0, 0.0, 0.0)
     extra: dict = field(default_factory=dict)
 
     def c(self) -> _Cfg:
@@ -129,6 +134,8 @@ class Config:
         s.ng = self.ng
         s.recon, s.riemann, s.rk_stages = self.recon, self.riemann, self.rk_stages
         s.gamma, s.cfl = self.gamma, self.cfl
+        for d in range(3):
+            s.grav[d] = self.grav[d]
         return s
 
     @property
@@ -210,6 +217,23 @@ def plm_face(wm1, w0, w1, w2):
 
 def weno5_edge(a, b, c, d, e) -> float:
     return lib().oracle_weno5_edge(a, b, c, d, e)
+
+
+def mc_face(wm1, w0, w1, w2):
+    l, r = ctypes.c_double(), ctypes.c_double()
+    lib().oracle_mc_face(wm1, w0, w1, w2, ctypes.byref(l), ctypes.byref(r))
+    return l.value, r.value
+
+
+def weno5z_edge(a, b, c, d, e) -> float:
+    return lib().oracle_weno5z_edge(a, b, c, d, e)
+
+
+def weno5z_face(s):
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    l, r = ctypes.c_double(), ctypes.c_double()
+    lib().oracle_weno5z_face(_dp(s), ctypes.byref(l), ctypes.byref(r))
+    return l.value, r.value
 
 
 def weno5_face(s):

@@ -14,7 +14,8 @@
  *     fill_guardcells() for all blocks, then for every block the block
  *     initialisation (Alg. 7: initSoln keeps U^n) and the
  *     intra-stage calculations (Alg. 8):
- *     grvAccel (identity, no gravity) -> calcLims (reconstruction) ->
+ *     grvAccel (uniform gravity source, NEXT N2; identity when g = 0) ->
+ *     calcLims (reconstruction: PLM-minmod / PLM-MC / WENO5-JS / WENO5-Z) ->
  *     calcFlux (Riemann) -> updSoln (divergence + RK combination) ->
  *     calcEos (pressure / positivity check).  fluxBuff is not needed on a
  *     single-level grid (no coarse-fine faces).
@@ -45,14 +46,15 @@ typedef struct {
     int32_t ng;
     double lo[3], hi[3];
     int32_t bc[3][2];       /* 0 periodic, 1 outflow, 2 reflect */
-    int32_t recon;          /* 0 first order, 1 PLM-minmod, 2 WENO5-JS */
+    int32_t recon;          /* 0 first order, 1 PLM-minmod, 2 WENO5-JS, 3 PLM-MC, 4 WENO5-Z */
     int32_t riemann;        /* 0 HLL, 1 HLLC */
     int32_t rk_stages;      /* 2 or 3 */
     double gamma, cfl;
+    double grav[3];         /* grvAccel: uniform gravitational acceleration (0: none) */
 } ocfg;
 
 enum { OBC_PERIODIC = 0, OBC_OUTFLOW = 1, OBC_REFLECT = 2 };
-enum { OREC_FIRST = 0, OREC_PLM = 1, OREC_WENO5 = 2 };
+enum { OREC_FIRST = 0, OREC_PLM = 1, OREC_WENO5 = 2, OREC_PLM_MC = 3, OREC_WENO5Z = 4 };
 enum { ORS_HLL = 0, ORS_HLLC = 1 };
 
 /* status codes */
@@ -60,6 +62,12 @@ enum { OK = 0, OERR_ARG = 1, OERR_NONPHYSICAL = 5, OERR_OOM = 4 };
 
 /* ---------------------------------------------------------------- geometry */
 static int nvar_of(const ocfg* c) { return c->ndim + 2; }
+/* reconstruction half-width (cells each side of a face the stencil reaches) */
+static int ngk_of(int recon) {
+    if (recon == OREC_WENO5 || recon == OREC_WENO5Z) return 3;
+    if (recon == OREC_PLM || recon == OREC_PLM_MC) return 2;
+    return 1;
+}
 static long cells_per_block(const ocfg* c) { return (long)c->nb[0] * c->nb[1] * c->nb[2]; }
 static long nblocks(const ocfg* c) { return (long)c->nblk[0] * c->nblk[1] * c->nblk[2]; }
 static int guard_of(const ocfg* c, int d) { return d < c->ndim ? c->ng : 0; }
@@ -79,8 +87,7 @@ int oracle_check_config(const ocfg* c) {
         if (d >= c->ndim && (c->nb[d] != 1 || c->nblk[d] != 1)) return OERR_ARG;
         if (d < c->ndim && c->nb[d] < c->ng) return OERR_ARG;
     }
-    int need = c->recon == OREC_WENO5 ? 3 : (c->recon == OREC_PLM ? 2 : 1);
-    if (c->recon < 0 || c->recon > 2 || c->ng < need) return OERR_ARG;
+    if (c->recon < 0 || c->recon > 4 || c->ng < ngk_of(c->recon)) return OERR_ARG;
     if (c->riemann < 0 || c->riemann > 1) return OERR_ARG;
     if (c->rk_stages != 2 && c->rk_stages != 3) return OERR_ARG;
     if (!(c->gamma > 1.0) || !(c->cfl > 0.0)) return OERR_ARG;
@@ -215,10 +222,55 @@ double oracle_weno5_edge(double a, double b, double c, double d, double e) {
     return (a0 * q0 + a1 * q1 + a2 * q2) / (a0 + a1 + a2);
 }
 
+/* Monotonized-central limiter (van Leer 1977; Toro 2009 §13.8, DESIGN.md
+ * reading R18): slope = minmod(2 dl, (dl + dr)/2, 2 dr), the three-argument
+ * minmod being 0 unless all three are strictly positive or all strictly
+ * negative, then the one of smallest magnitude. */
+static double minmod3(double a, double b, double c) {
+    if (a > 0.0 && b > 0.0 && c > 0.0) return fmin(a, fmin(b, c));
+    if (a < 0.0 && b < 0.0 && c < 0.0) return fmax(a, fmax(b, c));
+    return 0.0;
+}
+
+static double mc_slope(double wm, double w0, double wp) {
+    const double dl = w0 - wm, dr = wp - w0;
+    return minmod3(2.0 * dl, 0.5 * (dl + dr), 2.0 * dr);
+}
+
+/* PLM-MC face states at i+1/2 from W_{i-1}, W_i, W_{i+1}, W_{i+2}. */
+void oracle_mc_face(double wm1, double w0, double w1, double w2, double* wl, double* wr) {
+    *wl = w0 + 0.5 * mc_slope(wm1, w0, w1);
+    *wr = w1 - 0.5 * mc_slope(w0, w1, w2);
+}
+
+/* WENO5-Z (Borges, Carmona, Costa & Don 2008, eq. 25-26 with q = 1,
+ * eps = 1e-40; reading R19): the WENO5-JS smoothness indicators and
+ * candidates, weights alpha_k = d_k (1 + tau5 / (beta_k + eps)) with
+ * tau5 = |beta_0 - beta_2|; value at the right edge of cell c. */
+double oracle_weno5z_edge(double a, double b, double c, double d, double e) {
+    const double eps = 1e-40;
+    double b0 = 13.0 / 12.0 * (a - 2.0 * b + c) * (a - 2.0 * b + c) + 0.25 * (a - 4.0 * b + 3.0 * c) * (a - 4.0 * b + 3.0 * c);
+    double b1 = 13.0 / 12.0 * (b - 2.0 * c + d) * (b - 2.0 * c + d) + 0.25 * (b - d) * (b - d);
+    double b2 = 13.0 / 12.0 * (c - 2.0 * d + e) * (c - 2.0 * d + e) + 0.25 * (3.0 * c - 4.0 * d + e) * (3.0 * c - 4.0 * d + e);
+    double tau = fabs(b0 - b2);
+    double a0 = 0.1 * (1.0 + tau / (b0 + eps));
+    double a1 = 0.6 * (1.0 + tau / (b1 + eps));
+    double a2 = 0.3 * (1.0 + tau / (b2 + eps));
+    double q0 = (2.0 * a - 7.0 * b + 11.0 * c) / 6.0;
+    double q1 = (-b + 5.0 * c + 2.0 * d) / 6.0;
+    double q2 = (2.0 * c + 5.0 * d - e) / 6.0;
+    return (a0 * q0 + a1 * q1 + a2 * q2) / (a0 + a1 + a2);
+}
+
 /* WENO5 face states at i+1/2 from W_{i-2..i+3} (s[0..5]). */
 void oracle_weno5_face(const double* s, double* wl, double* wr) {
     *wl = oracle_weno5_edge(s[0], s[1], s[2], s[3], s[4]);
     *wr = oracle_weno5_edge(s[5], s[4], s[3], s[2], s[1]);
+}
+
+void oracle_weno5z_face(const double* s, double* wl, double* wr) {
+    *wl = oracle_weno5z_edge(s[0], s[1], s[2], s[3], s[4]);
+    *wr = oracle_weno5z_edge(s[5], s[4], s[3], s[2], s[1]);
 }
 
 /* Face states for all nvar primitive components.  st[m*nv + v] holds the
@@ -234,10 +286,13 @@ static void reconstruct(int recon, int ng, int nv, const double* st, double* wl,
             wr[v] = c1[v];
         } else if (recon == OREC_PLM) {
             oracle_plm_face(st[(ng - 2) * nv + v], c0[v], c1[v], st[(ng + 1) * nv + v], &wl[v], &wr[v]);
+        } else if (recon == OREC_PLM_MC) {
+            oracle_mc_face(st[(ng - 2) * nv + v], c0[v], c1[v], st[(ng + 1) * nv + v], &wl[v], &wr[v]);
         } else {
             double s[6];
             for (int m = 0; m < 6; m++) s[m] = st[(ng - 3 + m) * nv + v];
-            oracle_weno5_face(s, &wl[v], &wr[v]);
+            if (recon == OREC_WENO5) oracle_weno5_face(s, &wl[v], &wr[v]);
+            else oracle_weno5z_face(s, &wl[v], &wr[v]);
         }
     }
     if (!(wl[0] > 0.0) || !(wl[nv - 1] > 0.0) || !(wr[0] > 0.0) || !(wr[nv - 1] > 0.0)) {
@@ -247,6 +302,20 @@ static void reconstruct(int recon, int ng, int nv, const double* st, double* wl,
         }
     }
 }
+
+/* grvAccel (Alg. 8; reading R20): a uniform gravitational
+ * acceleration g enters the stage operator as the source
+ * S(U) = (0, rho g, m . g) evaluated at the stage's input state. */
+static double grav_source(const ocfg* c, int v, const double* u) {
+    const int nv = nvar_of(c);
+    if (v == 0) return 0.0;
+    if (v < nv - 1) return u[0] * c->grav[v - 1];
+    double s = 0.0;
+    for (int d = 0; d < c->ndim; d++) s += u[1 + d] * c->grav[d];
+    return s;
+}
+
+static int has_grav(const ocfg* c) { return c->grav[0] != 0.0 || c->grav[1] != 0.0 || c->grav[2] != 0.0; }
 
 /* ------------------------------------------------------------------ Riemann */
 /* Physical flux along the normal of the rotated frame (rho, u_n, u_t.., p).
@@ -418,7 +487,8 @@ int oracle_stage_padded(const ocfg* c, const double* P, const double* Un, double
                     for (int i = 0; i < c->nb[0]; i++) {
                         long cell = ((long)k * c->nb[1] + j) * c->nb[0] + i;
                         long pcell = ((long)(k + g[2]) * pn[1] + (j + g[1])) * pn[0] + (i + g[0]);
-                        double unew[5];
+                        double unew[5], uc[5];
+                        for (int v = 0; v < nv; v++) uc[v] = Pb[(long)v * NB * np + pcell];
                         for (int v = 0; v < nv; v++) {
                             double div[3] = {0.0, 0.0, 0.0};
                             for (int d = 0; d < ndim; d++) {
@@ -435,7 +505,8 @@ int oracle_stage_padded(const ocfg* c, const double* P, const double* Un, double
                             if (ndim == 1) L = -(div[0]);
                             else if (ndim == 2) L = -(div[0] + div[1]);
                             else L = -(div[0] + div[1]) - div[2];
-                            double uprev = Pb[(long)v * NB * np + pcell];
+                            if (has_grav(c)) L += grav_source(c, v, uc);  /* grvAccel */
+                            double uprev = uc[v];
                             double un = Un ? Un[(long)v * NB * nc + blk * nc + cell] : 0.0;
                             double val = a * un + b * (uprev + dt * L);
                             unew[v] = val;
@@ -547,7 +618,6 @@ int oracle_num_threads(void) {
  * evolved like any halo cell (reading R17).  With periodic boundaries the
  * result equals the non-telescoping step exactly (same arithmetic on the same
  * values).  dt as in oracle_step (CFL of U^n). */
-static int ngk_of(int recon) { return recon == OREC_WENO5 ? 3 : (recon == OREC_PLM ? 2 : 1); }
 
 int oracle_step_telescoping(const ocfg* c, double* U, double t, double t_end, double dt_fixed, double* dt_used) {
     if (oracle_check_config(c)) return OERR_ARG;
@@ -653,7 +723,8 @@ int oracle_step_telescoping(const ocfg* c, double* U, double t, double t_end, do
                     for (int j = lo[1]; j < hi[1]; j++)
                         for (int i = lo[0]; i < hi[0]; i++) {
                             long q = ((long)k * pn[1] + j) * pn[0] + i;
-                            double unew[5];
+                            double unew[5], uc[5];
+                            for (int v = 0; v < nv; v++) uc[v] = Tp[(long)v * np + q];
                             for (int v = 0; v < nv; v++) {
                                 double div[3] = {0.0, 0.0, 0.0};
                                 for (int d = 0; d < ndim; d++)
@@ -662,7 +733,8 @@ int oracle_step_telescoping(const ocfg* c, double* U, double t, double t_end, do
                                 if (ndim == 1) L = -(div[0]);
                                 else if (ndim == 2) L = -(div[0] + div[1]);
                                 else L = -(div[0] + div[1]) - div[2];
-                                unew[v] = a * T0[(long)v * np + q] + b * (Tp[(long)v * np + q] + dt * L);
+                                if (has_grav(c)) L += grav_source(c, v, uc);  /* grvAccel */
+                                unew[v] = a * T0[(long)v * np + q] + b * (uc[v] + dt * L);
                                 To[(long)v * np + q] = unew[v];
                             }
                             double w[5];

@@ -26,7 +26,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 BC_PERIODIC, BC_OUTFLOW, BC_REFLECT = 0, 1, 2
-RECON_FIRST, RECON_PLM, RECON_WENO5 = 0, 1, 2
+RECON_FIRST, RECON_PLM, RECON_WENO5, RECON_PLM_MC, RECON_WENO5Z = 0, 1, 2, 3, 4
 RIEMANN_HLL, RIEMANN_HLLC = 0, 1
 
 
@@ -49,11 +49,13 @@ class Problem:
     gamma: float = 1.4
     ic: str = "sod"
     t_end: float = 0.0
+    grav: tuple = (0.0, 0.0, 0.0)
 
     def config(self) -> dict:
         return dict(ndim=self.ndim, nb=tuple(self.nb), nblk=tuple(self.nblk), ng=self.ng, lo=tuple(self.lo),
                     hi=tuple(self.hi), bc=tuple(tuple(x) for x in self.bc), recon=self.recon,
-                    riemann=self.riemann, rk_stages=self.rk_stages, gamma=self.gamma, cfl=self.cfl)
+                    riemann=self.riemann, rk_stages=self.rk_stages, gamma=self.gamma, cfl=self.cfl,
+                    grav=tuple(self.grav))
 
     def with_(self, **kw) -> "Problem":
         return replace(self, **kw)
