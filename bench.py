@@ -151,8 +151,17 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml 10 ms"}
 
 
+RECONS = {"first": 0, "plm": 1, "weno5": 2, "mc": 3, "wenoz": 4}
+
+
 def problem_for(args, world: int) -> si.Problem:
     p = si.PRESETS[args.config]
+    if getattr(args, "recon", None):
+        r = RECONS[args.recon]
+        if r != p.recon:  # a different kernel: the committed ncu figures do not apply (name changes)
+            p = p.with_(name=f"{p.name}+{args.recon}", recon=r, ng=max(p.ng, 3 if r in (2, 4) else (2 if r in (1, 3) else 1)))
+    if getattr(args, "grav", None):
+        p = p.with_(grav=tuple(float(x) for x in args.grav.split(",")))
     if world > 1 and args.scaling == "weak":
         # weak scaling: 256^3 (16^3 blocks of 16^3) per GPU along a process grid
         pg = {2: (1, 1, 2), 4: (1, 2, 2), 8: (2, 2, 2)}.get(world)
@@ -228,6 +237,9 @@ def main():
     ap.add_argument("--telescoping", action="store_true",
                     help="telescoping SSP-RK steps (NEXT N1; 1-D/2-D, one rank): one launch per step")
     ap.add_argument("--impl", default="spark", choices=["spark", "reference"])
+    ap.add_argument("--recon", default=None, choices=["first", "plm", "weno5", "mc", "wenoz"],
+                    help="override the config's reconstruction (NEXT N2: mc = PLM-MC, wenoz = WENO5-Z)")
+    ap.add_argument("--grav", default=None, help="uniform gravity gx,gy,gz (grvAccel, NEXT N2)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = the config's grid per GPU; strong = the config's grid split over N")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -441,7 +453,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": p.name, "cells": p.ncells, "cells_per_gpu": cells_local,
-                       "block": list(p.nb), "blocks": list(p.nblk), "recon": ["first", "plm", "weno5"][p.recon],
+                       "block": list(p.nb), "blocks": list(p.nblk),
+                       "recon": ["first", "plm", "weno5", "plm_mc", "weno5z"][p.recon], "grav": list(p.grav),
                        "riemann": ["hll", "hllc"][p.riemann], "rk_stages": p.rk_stages, "ng": p.ng,
                        "parallelism": f"blocks over {world} GPU(s)", "l2": "state per copy > L2 (no flush needed)",
                        "rk_mode": "telescoping" if args.telescoping else "non-telescoping",

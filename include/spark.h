@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SPARK_ABI_VERSION 1
+#define SPARK_ABI_VERSION 2
 
 typedef enum {
     SPARK_OK = 0,
@@ -59,7 +59,15 @@ typedef enum {
 } spark_status;
 
 typedef enum { SPARK_BC_PERIODIC = 0, SPARK_BC_OUTFLOW = 1, SPARK_BC_REFLECT = 2 } spark_bc;
-typedef enum { SPARK_RECON_FIRST = 0, SPARK_RECON_PLM = 1, SPARK_RECON_WENO5 = 2 } spark_recon;
+/* PLM = minmod-limited (reading R2), WENO5 = WENO5-JS (R3); NEXT N2:
+ * PLM_MC = monotonized-central limiter (R18), WENO5Z = WENO5-Z (R19). */
+typedef enum {
+    SPARK_RECON_FIRST = 0,
+    SPARK_RECON_PLM = 1,
+    SPARK_RECON_WENO5 = 2,
+    SPARK_RECON_PLM_MC = 3,
+    SPARK_RECON_WENO5Z = 4
+} spark_recon;
 typedef enum { SPARK_RIEMANN_HLL = 0, SPARK_RIEMANN_HLLC = 1 } spark_riemann;
 
 /* Problem description.  Identical on every rank (it describes the GLOBAL grid). */
@@ -67,7 +75,7 @@ typedef struct {
     int32_t ndim;         /* 1..3; nvar = ndim + 2                                   */
     int32_t nb[3];        /* interior cells per block per dim (1 for d >= ndim)      */
     int32_t nblk[3];      /* blocks per dim of the global grid (1 for d >= ndim)     */
-    int32_t ng;           /* guard layers: >= 1 first order, >= 2 PLM, >= 3 WENO5    */
+    int32_t ng;           /* guard layers: >= 1 first order, >= 2 PLM(-MC), >= 3 WENO5(-Z) */
     double lo[3], hi[3];  /* domain; dx_d = (hi_d - lo_d) / (nblk_d * nb_d)          */
     int32_t bc[3][2];     /* spark_bc per face (low, high) per dim                   */
     int32_t recon;        /* spark_recon                                             */
@@ -75,6 +83,8 @@ typedef struct {
     int32_t rk_stages;    /* 2 (SSP-RK2) or 3 (SSP-RK3)                              */
     double gamma;         /* ideal-gas ratio of specific heats (> 1)                 */
     double cfl;           /* Courant number C in dt = C min dx_d/(|u_d| + c)         */
+    double grav[3];       /* grvAccel (Alg. 8; reading R20): uniform gravity;
+                           * L(U) += (0, rho g, m.g); all zero = no source. ABI v2  */
 } spark_config;
 
 typedef struct spark_ctx spark_ctx; /* opaque, one per rank (per GPU) */

@@ -44,13 +44,20 @@ struct Error : std::runtime_error {
             throw Error(SPARK_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));            \
     } while (0)
 
-int stencil_ng(int recon) { return recon == SPARK_RECON_WENO5 ? 3 : (recon == SPARK_RECON_PLM ? 2 : 1); }
+int stencil_ng(int recon) {
+    if (recon == SPARK_RECON_WENO5 || recon == SPARK_RECON_WENO5Z) return 3;
+    if (recon == SPARK_RECON_PLM || recon == SPARK_RECON_PLM_MC) return 2;
+    return 1;
+}
 
 std::string check(const spark_config* c, int nranks) {
     if (!c) return "null config";
     if (c->ndim < 1 || c->ndim > 3) return "ndim must be 1..3";
     if (nranks < 1) return "nranks must be >= 1";
-    if (c->recon < 0 || c->recon > 2) return "unknown recon";
+    if (c->recon < 0 || c->recon > 4) return "unknown recon";
+    for (int d = 0; d < 3; d++)
+        if (!std::isfinite(c->grav[d]) || (d >= c->ndim && c->grav[d] != 0.0))
+            return "grav must be finite and zero along unused dims";
     if (c->riemann < 0 || c->riemann > 1) return "unknown riemann";
     if (c->rk_stages != 2 && c->rk_stages != 3) return "rk_stages must be 2 or 3";
     if (!(c->gamma > 1.0)) return "gamma must be > 1";
@@ -179,6 +186,11 @@ Plan make_plan(const spark_config* c, int rank, int nranks, bool self_exchange =
     if (g.ncell >= (1LL << 31)) throw Error(SPARK_ERR_ARG, "sub-box exceeds 2^31 cells (split over more ranks)");
     g.gamma = c->gamma;
     g.cfl = c->cfl;
+    g.has_grav = 0;
+    for (int d = 0; d < 3; d++) {
+        g.grav[d] = c->grav[d];
+        if (c->grav[d] != 0.0) g.has_grav = 1;
+    }
     return p;
 }
 

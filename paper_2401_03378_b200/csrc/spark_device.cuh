@@ -24,7 +24,8 @@ constexpr int BC_PERIODIC = 0, BC_OUTFLOW = 1;  // BC_REFLECT = 2
 
 template <int RECON>
 struct StencilOf {
-    static constexpr int NG = RECON == 2 ? 3 : (RECON == 1 ? 2 : 1);  // cells each side of a face
+    // cells each side of a face: WENO5 / WENO5-Z 3, PLM / PLM-MC 2, first order 1
+    static constexpr int NG = (RECON == 2 || RECON == 4) ? 3 : ((RECON == 1 || RECON == 3) ? 2 : 1);
 };
 
 // ------------------------------------------------------------ arithmetic
@@ -104,6 +105,20 @@ __host__ __device__ __forceinline__ double minmod(double a, double b) {
     return (ia ^ ib) >= 0 ? dfrombits(r) : 0.0;
 }
 
+// Three-argument minmod (MC limiter, reading R18): 0 unless all three are
+// nonzero with the same sign, else the one of smallest magnitude (ties: the
+// later argument; the values are then equal).  Integer pipe, as minmod.
+__host__ __device__ __forceinline__ double minmod3(double a, double b, double c) {
+    const long long ia = dbits(a), ib = dbits(b), ic = dbits(c);
+    const unsigned long long ma = (unsigned long long)ia & 0x7fffffffffffffffull;
+    const unsigned long long mb = (unsigned long long)ib & 0x7fffffffffffffffull;
+    const unsigned long long mc = (unsigned long long)ic & 0x7fffffffffffffffull;
+    const long long rab = ma < mb ? ia : ib;
+    const unsigned long long mab = ma < mb ? ma : mb;
+    const long long r = mab < mc ? rab : ic;
+    return ((ia ^ ib) | (ia ^ ic)) >= 0 ? dfrombits(r) : 0.0;
+}
+
 // ------------------------------------------------------------------- EOS
 // Ideal gas (EOS unit): u = m/rho, p = (gamma-1)(E - m.u/2).
 // Returns false for rho <= 0, p <= 0 or non-finite p (calcEos check).
@@ -134,6 +149,40 @@ __host__ __device__ __forceinline__ void recon_cell(const double* s, double& lo,
         const double d = minmod(s[1] - s[0], s[2] - s[1]);
         lo = fma(-0.5, d, s[1]);
         hi = fma(0.5, d, s[1]);
+    } else if (RECON == 3) {  // PLM with the monotonized-central limiter (R18)
+        const double dl = s[1] - s[0], dr = s[2] - s[1];
+        const double d = minmod3(2.0 * dl, 0.5 * (dl + dr), 2.0 * dr);
+        lo = fma(-0.5, d, s[1]);
+        hi = fma(0.5, d, s[1]);
+    } else if (RECON == 4) {  // WENO5-Z (R19), both edges from shared indicators
+        // B_k = 4 beta_k as for JS; alpha_k = d_k (1 + tau/(beta_k + eps)) =
+        // d_k (D_k + T) / D_k with D_k = B_k + 4 eps, T = |B_0 - B_2|; multiplied
+        // through by 10 D_0 D_1 D_2 (one reciprocal per edge).  The left edge
+        // mirrors the stencils, i.e. swaps the roles of beta_0 and beta_2.
+        const double a = s[0], b = s[1], c = s[2], d = s[3], e = s[4];
+        constexpr double eps4 = 4e-40, k13 = 13.0 / 3.0;
+        const double t0 = fma(-2.0, b, a) + c, u0 = fma(3.0, c, fma(-4.0, b, a));
+        const double t1 = fma(-2.0, c, b) + d, u1 = b - d;
+        const double t2 = fma(-2.0, d, c) + e, u2 = fma(3.0, c, fma(-4.0, d, e));
+        const double B0 = fma(k13 * t0, t0, u0 * u0);
+        const double B1 = fma(k13 * t1, t1, u1 * u1);
+        const double B2 = fma(k13 * t2, t2, u2 * u2);
+        const double T = fabs(B0 - B2);
+        const double D0 = B0 + eps4, D1 = B1 + eps4, D2 = B2 + eps4;
+        const double P01 = D0 * D1, P02 = D0 * D2, P12 = D1 * D2;
+        const double A1 = 6.0 * ((D1 + T) * P02);
+        // right edge (i+1/2): (a,b,c), (b,c,d), (c,d,e) with weights 1 : 6 : 3
+        const double A0 = (D0 + T) * P12, A2 = 3.0 * ((D2 + T) * P01);
+        const double Q0 = fma(11.0, c, fma(-7.0, b, 2.0 * a));
+        const double Q1 = fma(2.0, d, fma(5.0, c, -b));
+        const double Q2 = fma(5.0, d, fma(2.0, c, -e));
+        hi = fma(A0, Q0, fma(A1, Q1, A2 * Q2)) * rcp(6.0 * (A0 + A1 + A2));
+        // left edge (i-1/2): (e,d,c), (d,c,b), (c,b,a): indicators beta_2, beta_1, beta_0
+        const double L0 = (D2 + T) * P01, L2 = 3.0 * ((D0 + T) * P12);
+        const double R0 = fma(11.0, c, fma(-7.0, d, 2.0 * e));
+        const double R1 = fma(2.0, b, fma(5.0, c, -d));
+        const double R2 = fma(5.0, b, fma(2.0, c, -a));
+        lo = fma(L0, R0, fma(A1, R1, L2 * R2)) * rcp(6.0 * (L0 + A1 + L2));
     } else {  // WENO5-JS, both edges from shared smoothness indicators
         // Same weights as the textbook form, regrouped for fewer FP64 operations:
         //   beta'_k = 4 beta_k = (13/3) t_k^2 + u_k^2,  (eps + beta)^2 = (4 eps + beta')^2 / 16
@@ -268,6 +317,22 @@ __host__ __device__ __forceinline__ void riemann(const double* wl, const double*
             for (int v = 0; v < NV; v++) f[v] = fma(slsr, UR[v] - UL[v], sr * FL[v] - sl * FR[v]) * inv;
         }
     }
+}
+
+// grvAccel source (reading R20) of variable v at a cell with conserved value u
+// of that variable, called in variable order: rho and m.g accumulate in
+// (rho, mg).  S = (0, rho g, m.g).
+template <int NV>
+__host__ __device__ __forceinline__ double grav_src(const Geo& g, int v, double u, double& rho, double& mg) {
+    if (v == 0) {
+        rho = u;
+        return 0.0;
+    }
+    if (v < NV - 1) {
+        mg = fma(u, g.grav[v - 1], mg);
+        return rho * g.grav[v - 1];
+    }
+    return mg;
 }
 
 // ------------------------------------------------------------ guard gather

@@ -37,6 +37,8 @@ struct Geo {
     long long slab[3];            // cells of one slab of dim d (ng * other extents)
     double dx[3], rdx[3];
     double gamma, cfl;
+    double grav[3];               // grvAccel source (reading R20)
+    int has_grav;                 // any grav[d] != 0
 };
 
 struct StageArgs {

@@ -43,7 +43,7 @@ constexpr int kThreads = 256;
 // (A 9th "boundary" warp doing all halo work was measured slower in 2-D and
 // 3-D — register cap 112 and a serial boundary critical path — DESIGN.md §4.2.)
 __host__ __device__ constexpr bool policy_stage_ops(int ndim, int recon, int nbx, int nby) {
-    return nbx == 16 && nby == 16 && ndim == 3 && recon <= 1;
+    return nbx == 16 && nby == 16 && ndim == 3 && (recon <= 1 || recon == 3);
 }
 
 template <int NV>
@@ -537,6 +537,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
         if (live) {
             const long long idx = cidx;
             double un[NV];
+            double grho = 0.0, gmg = 0.0;  // grvAccel accumulators (rho, m.g of U^(s-1))
 #pragma unroll
             for (int v = 0; v < NV; v++) {
                 const double dfx = (XA[v * fxn + tj * fxs + ti + 1] - XA[v * fxn + tj * fxs + ti]) * g.rdx[0];
@@ -557,6 +558,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                     u0 = u0v[v];
                     unn = unv[v];
                 }
+                if (g.has_grav) L += grav_src<NV>(g, v, u0, grho, gmg);
                 const double uo = fma(bco, fma(dt, L, u0), a * unn);
                 A.uout[v * ncell + idx] = uo;
                 un[v] = uo;
@@ -603,6 +605,8 @@ template <int NDIM>
 cudaError_t launch_d(const StageArgs& a, int recon, int riemann, cudaStream_t s) {
     if (recon == 0) return riemann ? launch_shape<NDIM, 0, 1>(a, s) : launch_shape<NDIM, 0, 0>(a, s);
     if (recon == 1) return riemann ? launch_shape<NDIM, 1, 1>(a, s) : launch_shape<NDIM, 1, 0>(a, s);
+    if (recon == 3) return riemann ? launch_shape<NDIM, 3, 1>(a, s) : launch_shape<NDIM, 3, 0>(a, s);
+    if (recon == 4) return riemann ? launch_shape<NDIM, 4, 1>(a, s) : launch_shape<NDIM, 4, 0>(a, s);
     return riemann ? launch_shape<NDIM, 2, 1>(a, s) : launch_shape<NDIM, 2, 0>(a, s);
 }
 
@@ -614,7 +618,7 @@ int stage_block_threads(const Geo& g, int /*recon*/) {
 }
 
 size_t stage_smem_bytes(const Geo& g, int recon) {
-    const int NG = recon == 2 ? 3 : (recon == 1 ? 2 : 1);
+    const int NG = (recon == 2 || recon == 4) ? 3 : ((recon == 1 || recon == 3) ? 2 : 1);
     const int NV = g.ndim + 2;
     const int nb0 = g.nb[0], nb1 = g.ndim >= 2 ? g.nb[1] : 1;
     const size_t P = (size_t)nb0 * nb1;

@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(kTeleThreads) telescope_kernel(const StageArgs
             const int i = lo + q % nux, j = loy + q / nux;
             const int c = j * tx + i;
             double un[NV];
+            double grho = 0.0, gmg = 0.0;  // grvAccel accumulators
 #pragma unroll
             for (int v = 0; v < NV; v++) {
                 const double dfx =
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(kTeleThreads) telescope_kernel(const StageArgs
                                        g.rdx[1];
                     L = -(dfx + dfy);
                 }
+                if (g.has_grav) L += grav_src<NV>(g, v, Tp[v * T + c], grho, gmg);
                 const double uo = fma(bco, fma(dt, L, Tp[v * T + c]), a * T0[v * T + c]);
                 un[v] = uo;
             }
@@ -193,13 +195,15 @@ template <int NDIM>
 cudaError_t launch_d(const StageArgs& a, int recon, int riemann, int S, cudaStream_t s) {
     if (recon == 0) return riemann ? launch_t<NDIM, 0, 1>(a, S, s) : launch_t<NDIM, 0, 0>(a, S, s);
     if (recon == 1) return riemann ? launch_t<NDIM, 1, 1>(a, S, s) : launch_t<NDIM, 1, 0>(a, S, s);
+    if (recon == 3) return riemann ? launch_t<NDIM, 3, 1>(a, S, s) : launch_t<NDIM, 3, 0>(a, S, s);
+    if (recon == 4) return riemann ? launch_t<NDIM, 4, 1>(a, S, s) : launch_t<NDIM, 4, 0>(a, S, s);
     return riemann ? launch_t<NDIM, 2, 1>(a, S, s) : launch_t<NDIM, 2, 0>(a, S, s);
 }
 
 }  // namespace
 
 size_t telescope_smem_bytes(const Geo& g, int recon, int S) {
-    const int NGK = recon == 2 ? 3 : (recon == 1 ? 2 : 1);
+    const int NGK = (recon == 2 || recon == 4) ? 3 : ((recon == 1 || recon == 3) ? 2 : 1);
     const int G = S * NGK;
     const size_t NV = g.ndim + 2;
     const size_t tx = g.nb[0] + 2 * G, ty = g.ndim >= 2 ? g.nb[1] + 2 * G : 1;

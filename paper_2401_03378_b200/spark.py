@@ -53,6 +53,7 @@ class CConfig(ctypes.Structure):
         ("rk_stages", ctypes.c_int32),
         ("gamma", ctypes.c_double),
         ("cfl", ctypes.c_double),
+        ("grav", ctypes.c_double * 3),
     ]
 
 
@@ -78,6 +79,8 @@ def to_cconfig(cfg: dict) -> CConfig:
     c.rk_stages = int(cfg.get("rk_stages", 2))
     c.gamma = float(cfg.get("gamma", 1.4))
     c.cfl = float(cfg.get("cfl", 0.8))
+    for d in range(3):
+        c.grav[d] = float(cfg.get("grav", (0.0,) * 3)[d])
     return c
 
 

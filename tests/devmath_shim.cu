@@ -20,9 +20,13 @@ void shim_riemann(int kind, int nv, int d, double gamma, const double* wl, const
     else if (nv == 4) kind ? rs_dispatch<4, 1>(d, gamma, wl, wr, f) : rs_dispatch<4, 0>(d, gamma, wl, wr, f);
     else kind ? rs_dispatch<5, 1>(d, gamma, wl, wr, f) : rs_dispatch<5, 0>(d, gamma, wl, wr, f);
 }
+double shim_minmod3(double a, double b, double c) { return minmod3(a, b, c); }
+
 void shim_recon(int recon, const double* s, double* lo, double* hi) {
     if (recon == 0) recon_cell<0>(s, *lo, *hi);
     else if (recon == 1) recon_cell<1>(s, *lo, *hi);
+    else if (recon == 3) recon_cell<3>(s, *lo, *hi);
+    else if (recon == 4) recon_cell<4>(s, *lo, *hi);
     else recon_cell<2>(s, *lo, *hi);
 }
 double shim_minmod(double a, double b) { return minmod(a, b); }

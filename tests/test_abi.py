@@ -32,7 +32,7 @@ def test_library_exports_every_symbol():
     L = spark.lib()
     for name in header_functions():
         assert hasattr(L, name), name
-    assert L.spark_abi_version() == 1
+    assert L.spark_abi_version() == 2
 
 
 def test_sm100a_code_in_library():
@@ -59,6 +59,16 @@ def test_config_rejections():
     assert not spark.check_config(base.with_(bc=((0, 1), (1, 1), (1, 1))).config())  # half periodic
     assert not spark.check_config(base.config(), 3)                               # 16 % 3 != 0
     assert spark.check_config(base.config(), 8)
+    # NEXT N2: MC (ng 2), WENO-Z (ng 3), gravity finite and zero along unused dims
+    assert spark.check_config(base.with_(recon=3).config())
+    assert not spark.check_config(base.with_(recon=4).config())
+    assert spark.check_config(base.with_(recon=4, ng=3).config())
+    assert not spark.check_config(base.with_(recon=5, ng=3).config())
+    assert spark.check_config(base.with_(grav=(0.1, -2.0, 3.0)).config())
+    assert not spark.check_config(base.with_(grav=(float("nan"), 0.0, 0.0)).config())
+    c2 = si.PRESETS["c2b_sod2d"]
+    assert spark.check_config(c2.with_(grav=(0.0, -1.0, 0.0)).config())
+    assert not spark.check_config(c2.with_(grav=(0.0, 0.0, -1.0)).config())
 
 
 @pytest.mark.parametrize("nranks", [1, 2, 4, 8])

@@ -64,11 +64,11 @@ def test_minmod_bitwise(shim):
             assert d == rule(a, b) and np.signbit(d) == np.signbit(rule(a, b)) or d == 0.0 == rule(a, b)
 
 
-@pytest.mark.parametrize("recon", [1, 2])
+@pytest.mark.parametrize("recon", [1, 2, 3, 4])
 def test_recon_cell_matches_faces(shim, recon):
     """Cell-centric edges == the oracle's per-face states."""
     g = np.random.Generator(np.random.PCG64(2))
-    R = recon  # stencil radius of the cell-centric form
+    R = 1 if recon in (1, 3) else 2  # stencil radius of the cell-centric form
     for _ in range(500):
         w = g.uniform(0.1, 2.0, 2 * R + 3) * np.where(g.random(2 * R + 3) < 0.3, 10.0, 1.0)
         # cell c = w[R+1]; its hi edge is W_L of face c+1/2, its lo edge is W_R of face c-1/2
@@ -76,14 +76,36 @@ def test_recon_cell_matches_faces(shim, recon):
         s = np.ascontiguousarray(w[c - R:c + R + 1])
         lo, hi = ctypes.c_double(), ctypes.c_double()
         shim.shim_recon(recon, _p(s), ctypes.byref(lo), ctypes.byref(hi))
-        if recon == 1:
-            oL, _ = oracle.plm_face(w[c - 1], w[c], w[c + 1], w[c + 2])
-            _, oR = oracle.plm_face(w[c - 2], w[c - 1], w[c], w[c + 1])
+        if recon in (1, 3):
+            face = oracle.plm_face if recon == 1 else oracle.mc_face
+            oL, _ = face(w[c - 1], w[c], w[c + 1], w[c + 2])
+            _, oR = face(w[c - 2], w[c - 1], w[c], w[c + 1])
             assert hi.value == oL and lo.value == oR  # bitwise (exact arithmetic)
         else:
-            oL = oracle.weno5_edge(*w[c - 2:c + 3])
-            oR = oracle.weno5_edge(*w[c + 2:c - 3:-1])
+            edge = oracle.weno5_edge if recon == 2 else oracle.weno5z_edge
+            oL = edge(*w[c - 2:c + 3])
+            oR = edge(*w[c + 2:c - 3:-1])
             assert abs(hi.value - oL) <= 1e-14 * abs(oL) and abs(lo.value - oR) <= 1e-14 * abs(oR)
+
+
+def test_minmod3_rule(shim):
+    """Integer-pipe three-argument minmod == the comparison form, incl. zeros."""
+    L = shim
+    L.shim_minmod3.argtypes = [ctypes.c_double] * 3
+    L.shim_minmod3.restype = ctypes.c_double
+
+    def rule(a, b, c):
+        if a > 0 and b > 0 and c > 0:
+            return min(a, b, c)
+        if a < 0 and b < 0 and c < 0:
+            return max(a, b, c)
+        return 0.0
+
+    g = np.random.Generator(np.random.PCG64(3))
+    vals = list(g.normal(size=60)) + [0.0, -0.0, 1.0, -1.0, 2.0, 1e-300, -1e-300]
+    for _ in range(20000):
+        a, b, c = (vals[i] for i in g.integers(0, len(vals), 3))
+        assert L.shim_minmod3(a, b, c) == rule(a, b, c)
 
 
 def _rot(W, d, ndim):
