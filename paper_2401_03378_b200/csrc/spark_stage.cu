@@ -536,30 +536,30 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
         // ---------------------------------------------------------------- S4
         if (live) {
             const long long idx = cidx;
-            double un[NV];
-            double grho = 0.0, gmg = 0.0;  // grvAccel accumulators (rho, m.g of U^(s-1))
+            double un[NV], Lv[NV];
 #pragma unroll
             for (int v = 0; v < NV; v++) {
                 const double dfx = (XA[v * fxn + tj * fxs + ti + 1] - XA[v * fxn + tj * fxs + ti]) * g.rdx[0];
-                double L;
                 if (NDIM == 1) {
-                    L = -dfx;
+                    Lv[v] = -dfx;
                 } else {
                     const double dfy = (YA[v * fyn + (tj + 1) * nb0 + ti] - YA[v * fyn + tj * nb0 + ti]) * g.rdx[1];
-                    if (NDIM == 2) L = -(dfx + dfy);
-                    else L = -(dfx + dfy) - (fzhi[v] - fzlo[v]) * g.rdx[2];
+                    if (NDIM == 2) Lv[v] = -(dfx + dfy);
+                    else Lv[v] = -(dfx + dfy) - (fzhi[v] - fzlo[v]) * g.rdx[2];
                 }
-                double u0, unn;
-                if (STAGE_OPS) {
-                    if (v == 0) cp_async_wait_all();
-                    u0 = stg[v * P + tid];
-                    unn = a != 0.0 ? stg[(NV + v) * P + tid] : 0.0;
-                } else {
-                    u0 = u0v[v];
-                    unn = unv[v];
-                }
-                if (g.has_grav) L += grav_src<NV>(g, v, u0, grho, gmg);
-                const double uo = fma(bco, fma(dt, L, u0), a * unn);
+            }
+            if (STAGE_OPS) cp_async_wait_all();
+            auto op_u0 = [&](int v) { return STAGE_OPS ? stg[v * P + tid] : u0v[v]; };
+            if (g.has_grav) {  // grvAccel source at U^(s-1) (CTA-uniform branch)
+                double grho = 0.0, gmg = 0.0;
+#pragma unroll
+                for (int v = 0; v < NV; v++) Lv[v] += grav_src<NV>(g, v, op_u0(v), grho, gmg);
+            }
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                const double u0 = op_u0(v);
+                const double unn = STAGE_OPS ? (a != 0.0 ? stg[(NV + v) * P + tid] : 0.0) : unv[v];
+                const double uo = fma(bco, fma(dt, Lv[v], u0), a * unn);
                 A.uout[v * ncell + idx] = uo;
                 un[v] = uo;
                 fzlo[v] = fzhi[v];
