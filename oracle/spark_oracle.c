@@ -470,12 +470,15 @@ int oracle_stage_padded(const ocfg* c, const double* P, const double* Un, double
                             /* face between cells (idx-1) and idx along d; padded coords
                              * of the cell on its right are (i,j,k)+g. */
                             long right = ((long)(k + g[2]) * pn[1] + (j + g[1])) * pn[0] + (i + g[0]);
+                            /* the stencil: 2 ngk cells around the face (ng >= ngk guard
+                             * layers exist; only the reconstruction's reach is read) */
+                            const int ngk = ngk_of(c->recon);
                             double st[6 * 5], wl[5], wr[5], fr[5];
-                            for (int m = 0; m < 2 * ng; m++) {
-                                long q = right + (long)(m - ng) * pstride[d];
+                            for (int m = 0; m < 2 * ngk; m++) {
+                                long q = right + (long)(m - ngk) * pstride[d];
                                 for (int v = 0; v < nv; v++) st[m * nv + v] = W[(long)rot[v] * np + q];
                             }
-                            reconstruct(c->recon, ng, nv, st, wl, wr);
+                            reconstruct(c->recon, ngk, nv, st, wl, wr);
                             riemann_ax(c->riemann, nv, c->gamma, ax, wl, wr, fr);
                             long fidx = ((long)k * fn[1] + j) * fn[0] + i;
                             for (int v = 0; v < nv; v++) F[d][(long)rot[v] * nf[d] + fidx] = fr[v];

@@ -200,3 +200,16 @@ def test_n2_config_validation():
     assert oracle.check_config(p.with_(recon=4, ng=2).config()) != 0      # WENO-Z needs ng 3
     assert oracle.check_config(p.with_(recon=4, ng=3).config()) == 0
     assert oracle.check_config(p.with_(recon=5, ng=3).config()) != 0
+
+
+@pytest.mark.parametrize("recon", [0, 1, 2, 3, 4])
+def test_extra_guard_layers_change_nothing(recon):
+    """ng beyond the reconstruction's reach (NGK) adds guard layers nobody
+    reads: the step is bitwise identical (regression: the oracle's stencil
+    buffer once held only 6 cells and overflowed for WENO with ng = 4)."""
+    ngk = 3 if recon in (2, 4) else (2 if recon in (1, 3) else 1)
+    p = si.Problem("xg", 2, (8, 8, 1), (2, 2, 1), ngk, recon, 1, 3, 0.4, bc=((2, 1), (0, 0), (1, 1)))
+    U0 = cons(p, si.random_state(p, 9, blocky=True))
+    a, _ = oracle.step(p.config(), U0)
+    b, _ = oracle.step(p.with_(ng=ngk + 1).config(), U0)
+    assert np.array_equal(a, b)
