@@ -13,7 +13,7 @@ import spark_inputs as si
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-NCASES = 40
+NCASES = 120
 
 
 def draw(i):
