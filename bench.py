@@ -366,6 +366,19 @@ def main():
                          "unit": "T FP64 instr/s", "frac": ach / fp64_peak,
                          "per_zone": fp64_per_zone, "source": "ncu instruction counts x live kernel time"}
 
+    # issue view: executed warp instructions per zone-update (ncu) x the kernel's
+    # zone rate, against the SM issue peak (4 schedulers x 1 warp-instr/clk x 148
+    # SMs at the sampled clock; B200_PROFILING.md unit counts)
+    roofline_issue = None
+    inst_per_zone = ncu_field(p.name, "inst_per_zone") or ncu_field(p.name.replace("c5_", "c4_"), "inst_per_zone")
+    if inst_per_zone:
+        zu_rate_kernel = cells_local * p.rk_stages * args.steps / (stage_ms * 1e-3)
+        clk_hz = (statistics.median(clk.samples) if clk.samples else 1965.0) * 1e6
+        peak_issue = 148 * 4 * clk_hz
+        ach = inst_per_zone / 32.0 * zu_rate_kernel
+        roofline_issue = {"bound": "issue", "achieved": ach / 1e12, "peak": peak_issue / 1e12,
+                          "unit": "T warp-instr/s", "frac": ach / peak_issue, "per_zone_thread_instr": inst_per_zone}
+
     # ---- end to end through the public API with host buffers
     e2e = None
     nbytes_state = int(np.prod(s.shape)) * 8
@@ -459,7 +472,7 @@ def main():
                        "parallelism": f"blocks over {world} GPU(s)", "l2": "state per copy > L2 (no flush needed)",
                        "rk_mode": "telescoping" if args.telescoping else "non-telescoping",
                        "launch": "cuda-graph (spark_run)" if args.graphs else "stream (spark_step)"},
-            "roofline": roofline, "roofline_fp64": roofline_fp64, "hbm_calibration_gbs": calib,
+            "roofline": roofline, "roofline_fp64": roofline_fp64, "roofline_issue": roofline_issue, "hbm_calibration_gbs": calib,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": total_launches,
             "clocks": clocks,
