@@ -215,6 +215,25 @@ __host__ __device__ __forceinline__ void recon_cell(const double* s, double& lo,
     }
 }
 
+// Face-centric first-order / PLM-type states at the face between cells i and
+// i+1 from W_{i-1..i+2}: W_L = hi edge of cell i, W_R = lo edge of cell i+1,
+// with the same formulas (hence bitwise the same values) as recon_cell.
+template <int RECON>
+__host__ __device__ __forceinline__ void face_states(double a, double b, double c, double d, double& wl,
+                                                     double& wr) {
+    if (RECON == 0) {  // first order: the cell values
+        wl = b;
+        wr = c;
+    } else if (RECON != 3) {  // minmod (the kernels call this for RECON 0, 1 and 3 only)
+        wl = fma(0.5, minmod(b - a, c - b), b);
+        wr = fma(-0.5, minmod(c - b, d - c), c);
+    } else {
+        const double l0 = b - a, r0 = c - b, r1 = d - c;
+        wl = fma(0.5, minmod3(2.0 * l0, 0.5 * (l0 + r0), 2.0 * r0), b);
+        wr = fma(-0.5, minmod3(2.0 * r0, 0.5 * (r0 + r1), 2.0 * r1), c);
+    }
+}
+
 // |u|^2 = (u_x^2 + u_y^2) + u_z^2: symmetric in u_x <-> u_y (bitwise), so a
 // face solved with swapped x/y components gives the identical flux.
 template <int NV>

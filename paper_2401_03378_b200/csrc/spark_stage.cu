@@ -45,6 +45,16 @@ constexpr int kThreads = 256;
 __host__ __device__ constexpr bool policy_stage_ops(int ndim, int recon, int nbx, int nby) {
     return nbx == 16 && nby == 16 && ndim == 3 && (recon <= 1 || recon == 3);
 }
+// Face-centric x/y reconstruction (3-D 16x16, first order / minmod PLM): the
+// thread that solves a face reconstructs both of its states straight from the
+// plane (two limiter evaluations per face instead of one per cell), so the
+// face-state arrays XB/YB, the halo edge-state pass and the S2->S3 barrier
+// disappear, and S3 solves one face at a time (no spills).
+__host__ __device__ constexpr bool policy_face_centric(int ndim, int recon, int nbx, int nby) {
+    // first order and minmod PLM (+16-20 %); MC measured 1 % slower, WENO5 would
+    // evaluate its edges twice
+    return nbx == 16 && nby == 16 && ndim == 3 && recon <= 1;
+}
 
 template <int NV>
 __device__ __forceinline__ void ldg_cons(const double* __restrict__ p, long long stride, double* u) {
@@ -62,7 +72,18 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int NDIM, int RECON, int RS, int NBX, int NBY>
 __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(const StageArgs A) {
     constexpr bool STAGE_OPS = policy_stage_ops(NDIM, RECON, NBX, NBY);
-    constexpr bool FUSE = NBX == 16 && NBY == 16 && NDIM == 3;  // paired face solves (S3)
+#ifdef EXP_NOFC
+    constexpr bool FC = false;
+#else
+    constexpr bool FC = policy_face_centric(NDIM, RECON, NBX, NBY);
+#endif
+    // paired face solves in S3 (WENO5 / first order); the face-centric path
+    // solves one face at a time (its reconstruction temporaries would spill)
+#ifdef EXP_NOFUSE
+    constexpr bool FUSE = false;
+#else
+    constexpr bool FUSE = NBX == 16 && NBY == 16 && NDIM == 3 && !FC;
+#endif
     constexpr int NV = NDIM + 2;
     constexpr int NG = StencilOf<RECON>::NG;
     constexpr int R = NG - 1;  // cell-centric reconstruction radius
@@ -95,10 +116,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     double* ring = smem;                       // [RING][NV][P]
     double* cur = ring + RING * NV * P;        // [NV][CP]
     double* XA = cur + NV * CP;                // [NV][fxn]: L state at x face, then x flux
-    double* XB = XA + NV * fxn;                // [NV][fxn]: R state at x face
-    double* YA = XB + NV * fxn;                // [NV][fyn]
-    double* YB = YA + NV * fyn;                // [NV][fyn]
-    double* stg = YB + NV * fyn;               // [2][NV][P] staged S4 operands (STAGE_OPS)
+    double* XB = XA + NV * fxn;                // [NV][fxn]: R state at x face (not with FC)
+    double* YA = XB + (FC ? 0 : NV * fxn);     // [NV][fyn]
+    double* YB = YA + NV * fyn;                // [NV][fyn] (not with FC)
+    double* stg = YB + (FC ? 0 : NV * fyn);    // [2][NV][P] staged S4 operands (STAGE_OPS)
 #ifdef ABL_NOHALO
     for (int q = threadIdx.x; q < NV * CP; q += blockDim.x) cur[q] = 1.0;
     __syncthreads();
@@ -331,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 }
             }
         }
-        if (live) {
+        if (live && !FC) {
 #pragma unroll
             for (int v = 0; v < NV; v++) {
                 double s[2 * R + 1], lo, hi;
@@ -349,14 +370,14 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                     YA[v * fyn + (tj + 1) * nb0 + ti] = hi;
                 }
             }
-            if (NDIM == 3) zrecon(kk + 1, zlo, zhn);
         }
+        if (live && NDIM == 3) zrecon(kk + 1, zlo, zhn);
         // edge states from the halo cells: one (cell, variable) item per thread
         // round so the extra work spreads over all warps
 #ifdef ABL_NOEDGE
         if (false)
 #endif
-        for (int qv = tid; qv < nbr * NV; qv += blockDim.x) {
+        for (int qv = tid; !FC && qv < nbr * NV; qv += blockDim.x) {
             const int v = qv / nbr, q = qv - v * nbr;
             const bool xd = q < 2 * nb1;
             const int qq = xd ? q : q - 2 * nb1;
@@ -381,15 +402,20 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 else YA[v * fyn + r] = hi;
             }
         }
-        __syncthreads();
+        if (!FC) __syncthreads();
         // ---------------------------------------------------------------- S3
         // x face at column f of row r: cells (f-1, f); y face at row f of column r
         auto xface = [&](int r, int f) {
             double wl[NV], wr[NV], fl[NV];
 #pragma unroll
             for (int v = 0; v < NV; v++) {
-                wl[v] = XA[v * fxn + r * fxs + f];
-                wr[v] = XB[v * fxn + r * fxs + f];
+                if (FC) {
+                    const double* c = cur + v * CP + (r + RO) * cw + f + NG;  // cell f
+                    face_states<RECON>(c[-2], c[-1], c[0], c[1], wl[v], wr[v]);
+                } else {
+                    wl[v] = XA[v * fxn + r * fxs + f];
+                    wr[v] = XB[v * fxn + r * fxs + f];
+                }
             }
             if (RECON != 0 && !(positive(wl[0]) && positive(wl[NV - 1]) && positive(wr[0]) && positive(wr[NV - 1]))) {
 #pragma unroll
@@ -406,8 +432,13 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             double wl[NV], wr[NV], fl[NV];
 #pragma unroll
             for (int v = 0; v < NV; v++) {
-                wl[v] = YA[v * fyn + f * nb0 + r];
-                wr[v] = YB[v * fyn + f * nb0 + r];
+                if (FC) {
+                    const double* c = cur + v * CP + (f + NG) * cw + r + NG;  // cell f of column r
+                    face_states<RECON>(c[-2 * cw], c[-cw], c[0], c[cw], wl[v], wr[v]);
+                } else {
+                    wl[v] = YA[v * fyn + f * nb0 + r];
+                    wr[v] = YB[v * fyn + f * nb0 + r];
+                }
             }
             if (RECON != 0 && !(positive(wl[0]) && positive(wl[NV - 1]) && positive(wr[0]) && positive(wr[NV - 1]))) {
 #pragma unroll
@@ -431,10 +462,16 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             double xl[NV], xr[NV], yl[NV], yr[NV], fx[NV], fy[NV];
 #pragma unroll
             for (int v = 0; v < NV; v++) {
-                xl[v] = XA[v * fxn + xo];
-                xr[v] = XB[v * fxn + xo];
-                yl[v] = YA[v * fyn + yo];
-                yr[v] = YB[v * fyn + yo];
+                if (FC) {  // x face ti+1 from cells ti-1..ti+2, y face tj+1 from tj-1..tj+2
+                    const double* c = cur + v * CP + (tj + RO) * cw + ti + NG;
+                    face_states<RECON>(c[-1], c[0], c[1], c[2], xl[v], xr[v]);
+                    face_states<RECON>(c[-cw], c[0], c[cw], c[2 * cw], yl[v], yr[v]);
+                } else {
+                    xl[v] = XA[v * fxn + xo];
+                    xr[v] = XB[v * fxn + xo];
+                    yl[v] = YA[v * fyn + yo];
+                    yr[v] = YB[v * fyn + yo];
+                }
             }
             if (RECON != 0) {
                 const bool nx = !(positive(xl[0]) && positive(xl[NV - 1]) && positive(xr[0]) && positive(xr[NV - 1]));
@@ -481,8 +518,14 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 double bl[NV], br[NV], fb[NV];
 #pragma unroll
                 for (int v = 0; v < NV; v++) {
-                    bl[v] = isy ? YA[v * fyn + q] : XA[v * fxn + q * fxs];
-                    br[v] = isy ? YB[v * fyn + q] : XB[v * fxn + q * fxs];
+                    if (FC) {  // face 0 of row / column q from cells -2..1
+                        const double* c = cur + v * CP + (isy ? NG * cw + q + NG : (q + RO) * cw + NG);
+                        const int st = isy ? cw : 1;
+                        face_states<RECON>(c[-2 * st], c[-st], c[0], c[st], bl[v], br[v]);
+                    } else {
+                        bl[v] = isy ? YA[v * fyn + q] : XA[v * fxn + q * fxs];
+                        br[v] = isy ? YB[v * fyn + q] : XB[v * fxn + q * fxs];
+                    }
                 }
                 if (RECON != 0 && !(positive(bl[0]) && positive(bl[NV - 1]) && positive(br[0]) && positive(br[NV - 1]))) {
 #pragma unroll
@@ -527,9 +570,50 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                     for (int v = 0; v < NV; v++) zhi[v] = zhn[v];
                 }
             }
-            for (int q = tid; q < nbf; q += blockDim.x) {
-                if (q < nb1) xface(q, 0);
-                else yface(q - nb1, 0);
+            if (FC && NBX == 16 && NBY == 16) {
+                // warp 0: the 32 block-boundary faces in one pass (y faces in the
+                // x frame with u_x <-> u_y swapped, bitwise identical; see FUSE)
+                if (tid < 32) {
+                    const bool isy = tid >= 16;
+                    const int q = tid & 15;
+                    double bl[NV], br[NV], fb[NV];
+#pragma unroll
+                    for (int v = 0; v < NV; v++) {
+                        const double* c = cur + v * CP + (isy ? NG * cw + q + NG : (q + RO) * cw + NG);
+                        const int st = isy ? cw : 1;
+                        face_states<RECON>(c[-2 * st], c[-st], c[0], c[st], bl[v], br[v]);
+                    }
+                    if (!(positive(bl[0]) && positive(bl[NV - 1]) && positive(br[0]) && positive(br[NV - 1]))) {
+#pragma unroll
+                        for (int v = 0; v < NV; v++) {
+                            bl[v] = isy ? cur[v * CP + (NG - 1) * cw + q + NG] : cur[v * CP + (q + RO) * cw + NG - 1];
+                            br[v] = isy ? cur[v * CP + NG * cw + q + NG] : cur[v * CP + (q + RO) * cw + NG];
+                        }
+                    }
+                    {
+                        const double l1 = bl[1], r1 = br[1];
+                        bl[1] = isy ? bl[2] : l1;
+                        bl[2] = isy ? l1 : bl[2];
+                        br[1] = isy ? br[2] : r1;
+                        br[2] = isy ? r1 : br[2];
+                    }
+                    riemann<NV, RS, 0>(bl, br, gamma, gm1i, fb);
+                    {
+                        const double f1 = fb[1];
+                        fb[1] = isy ? fb[2] : f1;
+                        fb[2] = isy ? f1 : fb[2];
+                    }
+#pragma unroll
+                    for (int v = 0; v < NV; v++) {
+                        if (isy) YA[v * fyn + q] = fb[v];
+                        else XA[v * fxn + q * fxs] = fb[v];
+                    }
+                }
+            } else {
+                for (int q = tid; q < nbf; q += blockDim.x) {
+                    if (q < nb1) xface(q, 0);
+                    else yface(q - nb1, 0);
+                }
             }
         }
         __syncthreads();
@@ -626,9 +710,14 @@ size_t stage_smem_bytes(const Geo& g, int recon) {
     const size_t ring = g.ndim == 3 ? slots * NV * P : 0;
     const size_t cw = nb0 + 2 * NG, ch = g.ndim >= 2 ? nb1 + 2 * NG : 1;
     const size_t cur = NV * cw * ch;
-    const size_t fx = 2 * NV * (size_t)(nb0 + 1) * nb1;
-    const size_t fy = g.ndim >= 2 ? 2 * NV * (size_t)nb0 * (nb1 + 1) : 0;
     const bool k16 = g.ndim >= 2 && nb0 == 16 && nb1 == 16;
+#ifdef EXP_NOFC
+    const size_t nst = 2;
+#else
+    const size_t nst = k16 && policy_face_centric(g.ndim, recon, 16, 16) ? 1 : 2;  // FC: fluxes only
+#endif
+    const size_t fx = nst * NV * (size_t)(nb0 + 1) * nb1;
+    const size_t fy = g.ndim >= 2 ? nst * NV * (size_t)nb0 * (nb1 + 1) : 0;
     const size_t stg = k16 && policy_stage_ops(g.ndim, recon, 16, 16) ? 2 * NV * P : 0;
     return (ring + cur + fx + fy + stg) * sizeof(double);
 }
