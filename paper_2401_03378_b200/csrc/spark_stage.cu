@@ -120,6 +120,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     double* YA = XB + (FC ? 0 : NV * fxn);     // [NV][fyn]
     double* YB = YA + NV * fyn;                // [NV][fyn] (not with FC)
     double* stg = YB + (FC ? 0 : NV * fyn);    // [2][NV][P] staged S4 operands (STAGE_OPS)
+    // FC in 3-D: the next plane's raw halo cells arrive by cp.async in shared
+    // memory (no prefetch registers held across the plane)
+    constexpr bool HSM = FC && NDIM == 3 && STAGE_OPS;
+    double* hs = stg + (STAGE_OPS ? 2 * NV * P : 0);  // [NV][nh]
 #ifdef ABL_NOHALO
     for (int q = threadIdx.x; q < NV * CP; q += blockDim.x) cur[q] = 1.0;
     __syncthreads();
@@ -272,7 +276,13 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             hp = s0.p;
             hvs = (int)s0.vs;
             hzf = (int)((s1.p - s0.p) * 16) | s0.flip;
-            load_src<NV>(hp, hvs, s0.flip, hpre);
+            if (HSM) {
+#pragma unroll
+                for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + tid, hp + (long long)v * hvs);
+                cp_async_commit();
+            } else {
+                load_src<NV>(hp, hvs, s0.flip, hpre);
+            }
         } else {  // one plane: a single load through the block-neighbour fast path
             load_cons(hcx, hcy, 0, hpre);
         }
@@ -315,8 +325,25 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
         if (HPF) {  // one halo cell per thread, prefetched one plane ahead
             if (hact) {
                 double w[NV];
-                ok &= cons_to_prim<NV>(hpre, w, gm1);
-                if (kk + 1 < nb2) load_halo(kk + 1, hpre);
+                if (HSM) {
+                    cp_async_wait_all();
+#pragma unroll
+                    for (int v = 0; v < NV; v++) hpre[v] = hs[v * nh + tid];
+#pragma unroll
+                    for (int d = 0; d < NV - 2; d++)  // reflecting-boundary image: momentum sign
+                        hpre[1 + d] = __hiloint2double(__double2hiint(hpre[1 + d]) ^ (((hzf >> (1 + d)) & 1) << 31),
+                                                       __double2loint(hpre[1 + d]));
+                    ok &= cons_to_prim<NV>(hpre, w, gm1);
+                    if (kk + 1 < nb2) {
+                        const double* src = hp + (long long)(kk + 1) * (hzf >> 4);
+#pragma unroll
+                        for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + tid, src + (long long)v * hvs);
+                        cp_async_commit();
+                    }
+                } else {
+                    ok &= cons_to_prim<NV>(hpre, w, gm1);
+                    if (kk + 1 < nb2) load_halo(kk + 1, hpre);
+                }
 #pragma unroll
                 for (int v = 0; v < NV; v++) cur[v * CP + (hcy + RO) * cw + hcx + NG] = w[v];
             }
@@ -719,7 +746,9 @@ size_t stage_smem_bytes(const Geo& g, int recon) {
     const size_t fx = nst * NV * (size_t)(nb0 + 1) * nb1;
     const size_t fy = g.ndim >= 2 ? nst * NV * (size_t)nb0 * (nb1 + 1) : 0;
     const size_t stg = k16 && policy_stage_ops(g.ndim, recon, 16, 16) ? 2 * NV * P : 0;
-    return (ring + cur + fx + fy + stg) * sizeof(double);
+    const size_t nh = 2 * (size_t)NG * (nb0 + nb1);
+    const size_t hsm = k16 && g.ndim == 3 && nst == 1 && stg ? NV * nh : 0;  // HSM staging
+    return (ring + cur + fx + fy + stg + hsm) * sizeof(double);
 }
 
 cudaError_t launch_stage(const StageArgs& a, int recon, int riemann, cudaStream_t s) {
