@@ -16,6 +16,8 @@
 //             the pool, L2-resident; no guard cells are stored in HBM)
 //   S2 recon  cell-centric: each cell's x, y (and z, from the ring) limiter /
 //             smoothness evaluation is done once and gives both edge states
+//             (face-centric variant, 16x16 first order / minmod PLM: x/y states
+//             are built in S3 by the face's own thread; no S2->S3 barrier)
 //   S3 flux   each face once: x/y faces into shared memory, the z face in
 //             registers (carried to the next plane)
 //   S4 update own cell; last stage also the CFL-min epilogue.
