@@ -92,31 +92,32 @@ __host__ __device__ __forceinline__ double dfrombits(long long b) {
 #endif
 }
 
+// Same-sign test on the sign bits (a zero counts with its sign; a kept signed
+// zero turns W +- d/2 into W exactly, as +0 does).
+__host__ __device__ __forceinline__ bool same_sign(double a, double b) {
+#ifdef __CUDA_ARCH__
+    return (__double2hiint(a) ^ __double2hiint(b)) >= 0;
+#else
+    return (dbits(a) ^ dbits(b)) >= 0;
+#endif
+}
+
 // minmod(a, b): 0 unless a and b are both nonzero with the same sign, else the
-// one of smaller magnitude (ties: b).  Integer pipe only (no DSETP / fmin NaN
-// handling): magnitudes compare as unsigned bit patterns.  Bitwise equal to
-// the oracle's comparison form (reading R2); a kept zero is signed,
-// which W +- d/2 turns into W exactly, as +0 does.
+// one of smaller magnitude (ties: b).  One DSETP on |a|, |b| (no fmin NaN
+// fix-ups), a sign-bit test and selects: 7 SASS instructions.  Bitwise equal
+// to the oracle's comparison form (reading R2).
 __host__ __device__ __forceinline__ double minmod(double a, double b) {
-    const long long ia = dbits(a), ib = dbits(b);
-    const unsigned long long ma = (unsigned long long)ia & 0x7fffffffffffffffull;
-    const unsigned long long mb = (unsigned long long)ib & 0x7fffffffffffffffull;
-    const long long r = ma < mb ? ia : ib;
-    return (ia ^ ib) >= 0 ? dfrombits(r) : 0.0;
+    const double r = fabs(a) < fabs(b) ? a : b;
+    return same_sign(a, b) ? r : 0.0;
 }
 
 // Three-argument minmod (MC limiter, reading R18): 0 unless all three are
 // nonzero with the same sign, else the one of smallest magnitude (ties: the
-// later argument; the values are then equal).  Integer pipe, as minmod.
+// later argument; the values are then equal).
 __host__ __device__ __forceinline__ double minmod3(double a, double b, double c) {
-    const long long ia = dbits(a), ib = dbits(b), ic = dbits(c);
-    const unsigned long long ma = (unsigned long long)ia & 0x7fffffffffffffffull;
-    const unsigned long long mb = (unsigned long long)ib & 0x7fffffffffffffffull;
-    const unsigned long long mc = (unsigned long long)ic & 0x7fffffffffffffffull;
-    const long long rab = ma < mb ? ia : ib;
-    const unsigned long long mab = ma < mb ? ma : mb;
-    const long long r = mab < mc ? rab : ic;
-    return ((ia ^ ib) | (ia ^ ic)) >= 0 ? dfrombits(r) : 0.0;
+    const double rab = fabs(a) < fabs(b) ? a : b;
+    const double r = fabs(rab) < fabs(c) ? rab : c;
+    return same_sign(a, b) && same_sign(a, c) ? r : 0.0;
 }
 
 // ------------------------------------------------------------------- EOS
