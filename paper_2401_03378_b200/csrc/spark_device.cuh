@@ -80,7 +80,9 @@ __host__ __device__ __forceinline__ long long dbits(double x) {
 #endif
 }
 
-__host__ __device__ __forceinline__ bool positive(double x) { return dbits(x) > 0; }
+// x > 0 (false for NaN, as the oracle's positivity fallback test): one DSETP,
+// where the integer form on the bit pattern needs a 64-bit compare (2 ISETP)
+__host__ __device__ __forceinline__ bool positive(double x) { return x > 0.0; }
 
 __host__ __device__ __forceinline__ double dfrombits(long long b) {
 #ifdef __CUDA_ARCH__
