@@ -279,32 +279,27 @@ __host__ __device__ __forceinline__ void riemann(const double* wl, const double*
         for (int v = 0; v < NV; v++) w[v] = left ? wl[v] : wr[v];
         const double sk = left ? sl : sr, qk = left ? ql : qr;
         const double rho = w[0], un = w[N], p = w[NV - 1];
-        const double irho = rcp(rho);
-        const double u2 = vsq<NV>(w);
-        const double E = fma(0.5 * rho, u2, p * gm1i);
-        const double mflux = rho * un;
-        f[0] = mflux;
+        const double E = fma(0.5 * rho, vsq<NV>(w), p * gm1i);
+        // F*_K = F_K + S_K (U*_K - U_K) (Toro §10.4) multiplied out with
+        // z = (S* - u_K)/(S_K - S*) and t = S_K z (so rho*_K = rho_K (1 + z)):
+        //   mass      rho_K (u_K + t)                       = F0
+        //   normal    F0 u_K + t q_K + p_K                  (q_K = rho_K (S_K - u_K))
+        //   transv.   F0 w_t
+        //   energy    (E_K + p_K)(u_K + t) + t q_K S*
+        // Outside the star region t = 0 gives F_K.  Branch-free: t is zeroed by
+        // one select after it is formed (a discarded value may be non-finite for
+        // a supersonic face), so no reciprocal of rho_K or q_K is needed.
+        const bool star = !lpos && !rneg;
+        const double z = (sstar - un) * rcp(sk - sstar);
+        const double t = star ? sk * z : 0.0;
+        const double v = un + t;
+        const double m = rho * v;
+        f[0] = m;
 #pragma unroll
-        for (int d = 1; d < NV - 1; d++) f[d] = mflux * w[d];
-        f[N] += p;
-        f[NV - 1] = un * (E + p);
-        // star-state correction F*_K = F_K + S_K (U*_K - U_K), applied by select
-        // (branch-free, so independent faces interleave; a discarded value may be
-        // non-finite for supersonic faces, which the select never propagates)
-        {
-            const bool star = !lpos && !rneg;
-            const double fac = qk * rcp(sk - sstar);
-            const double es = fma(sstar - un, fma(p, rcp(qk), sstar), E * irho);
-            const double c0 = fma(sk, fac - rho, f[0]);
-            f[0] = star ? c0 : f[0];
-#pragma unroll
-            for (int d = 1; d < NV - 1; d++) {
-                const double cd = fma(sk, fma(fac, d == N ? sstar : w[d], -rho * w[d]), f[d]);
-                f[d] = star ? cd : f[d];
-            }
-            const double ce = fma(sk, fma(fac, es, -E), f[NV - 1]);
-            f[NV - 1] = star ? ce : f[NV - 1];
-        }
+        for (int d = 1; d < NV - 1; d++) f[d] = m * w[d];
+        f[N] = fma(m, un, fma(t, qk, p));
+        const double ep = E + p;
+        f[NV - 1] = fma(ep, v, (t * qk) * sstar);
     } else {
         const double u2l = vsq<NV>(wl), u2r = vsq<NV>(wr);
         const double El = fma(0.5 * rl, u2l, pl * gm1i), Er = fma(0.5 * rr, u2r, pr * gm1i);
