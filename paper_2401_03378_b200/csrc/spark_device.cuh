@@ -110,7 +110,19 @@ __host__ __device__ __forceinline__ bool same_sign(double a, double b) {
 // to the oracle's comparison form (reading R2).
 __host__ __device__ __forceinline__ double minmod(double a, double b) {
     const double r = fabs(a) < fabs(b) ? a : b;
+#ifdef __CUDA_ARCH__
+    // sign test as one LOP3 with a predicate output ((hi(a) ^ hi(b)) & 2^31),
+    // which nvcc does not form from the C expression (it emits LOP3 + ISETP)
+    double out;
+    asm("{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\tsetp.eq.u32 q, 1, 1;\n\t"
+        "lop3.or.b32 t|p, %1, %2, 0x80000000, 0x28, !q;\n\t"
+        "selp.f64 %0, 0d0000000000000000, %3, p;\n\t}"
+        : "=d"(out)
+        : "r"(__double2hiint(a)), "r"(__double2hiint(b)), "d"(r));
+    return out;
+#else
     return same_sign(a, b) ? r : 0.0;
+#endif
 }
 
 // Three-argument minmod (MC limiter, reading R18): 0 unless all three are
@@ -138,7 +150,9 @@ __host__ __device__ __forceinline__ bool cons_to_prim(const double* u, double* w
     w[0] = rho;
     const double p = gm1 * fma(-0.5, ke, u[NV - 1]);
     w[NV - 1] = p;
-    return rho > 0.0 && p > 0.0 && p < INFINITY;
+    // p <= DBL_MAX rather than p < INFINITY: a chain of three DSETP, where the
+    // latter is compiled into ~10 integer instructions
+    return (rho > 0.0) & (p > 0.0) & (p <= 1.7976931348623157e308);
 }
 
 // -------------------------------------------------------- reconstruction
