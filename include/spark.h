@@ -21,6 +21,8 @@
  *                  lexicographic over THIS RANK's sub-box of the block grid.
  *       padded     P[v][b][k+gz][j+gy][i+gx], gd = ng for d < ndim else 0
  *                  (the Flash-X block-with-guards of P:361-364).
+ *     Internally the state is block-interleaved, U[b][v][k][j][i] (one block
+ *     is one contiguous chunk of HBM); set/get convert.
  *     v = 0 density, 1..ndim momentum, ndim+1 total energy (conserved) or
  *     v = 0 density, 1..ndim velocity, ndim+1 pressure (primitive).
  *   - Memory ownership: the CALLER owns the device arena passed to spark_init
@@ -236,7 +238,9 @@ spark_status spark_step_group(spark_ctx* const* ctxs, int32_t n, double dt, doub
  *   U_out = a * U_n + b * (U_prev + dt * L(U_prev))
  * with guard cells of U_prev from the boundary maps (single-rank contexts
  * only).  U_n may be NULL when a == 0.  For testing the stage in isolation.
- * Asynchronous. */
+ * The buffers are converted to and from the internal layout through the
+ * context's state buffers, so a loaded state is discarded (load a new one
+ * before stepping).  Asynchronous. */
 spark_status spark_stage_apply(spark_ctx* ctx, const double* U_prev, const double* U_n, double a, double b,
                                double dt, double* U_out);
 

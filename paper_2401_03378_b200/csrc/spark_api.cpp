@@ -162,6 +162,8 @@ Plan make_plan(const spark_config* c, int rank, int nranks, bool self_exchange =
             g.halo[d][s] = 0;
         }
     }
+    g.vs = g.cpb;
+    g.bs = (long long)g.nvar * g.cpb;
     for (int d = 0; d < c->ndim; d++) {
         for (int s = 0; s < 2; s++) {
             int q[3] = {p.pc[0], p.pc[1], p.pc[2]};
@@ -644,8 +646,13 @@ spark_status spark_set_state(spark_ctx* ctx, const double* U, int32_t on_device)
         set_device(ctx);
         const size_t bytes = sizeof(double) * ctx->plan.geo.nvar * (size_t)ctx->plan.geo.ncell;
         ctx->n_idx = 0;
-        CU(cudaMemcpyAsync(ctx->U[0], U, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                           ctx->stream));
+        const double* src = U;
+        if (!on_device) {  // stage through U[1] (dead before the first step)
+            CU(cudaMemcpyAsync(ctx->U[1], U, bytes, cudaMemcpyHostToDevice, ctx->stream));
+            src = ctx->U[1];
+        }
+        // canonical U[v][b][c] -> the block-interleaved pool U[b][v][c]
+        launched(ctx, spark::launch_relayout(ctx->plan.geo, src, ctx->U[0], 1, ctx->stream), "relayout");
         after_state_loaded(ctx);
     });
 }
@@ -672,8 +679,11 @@ spark_status spark_get_state(spark_ctx* ctx, double* U, int32_t on_device) {
         if (!ctx->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
         set_device(ctx);
         const size_t bytes = sizeof(double) * ctx->plan.geo.nvar * (size_t)ctx->plan.geo.ncell;
-        CU(cudaMemcpyAsync(U, ctx->U[ctx->n_idx], bytes,
-                           on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+        // block-interleaved pool -> canonical; a host copy stages through a state
+        // buffer that is dead between API calls (rollback happens inside spark_step)
+        double* dst = on_device ? U : ctx->U[(ctx->n_idx + 1) % 3];
+        launched(ctx, spark::launch_relayout(ctx->plan.geo, ctx->U[ctx->n_idx], dst, 0, ctx->stream), "relayout");
+        if (!on_device) CU(cudaMemcpyAsync(U, dst, bytes, cudaMemcpyDeviceToHost, ctx->stream));
         sync_and_check(ctx, false, -1);
     });
 }
@@ -825,7 +835,14 @@ spark_status spark_stage_apply(spark_ctx* ctx, const double* U_prev, const doubl
             throw Error(SPARK_ERR_STATE, "spark_stage_apply needs a single-rank context without NCCL exchange");
         if (a != 0.0 && !U_n) throw Error(SPARK_ERR_ARG, "U_n required when a != 0");
         set_device(ctx);
-        stage_launch(ctx, U_prev, U_n, a, b, U_out, false, nullptr, dt, false);
+        // the kernel runs on the block-interleaved layout: the caller's canonical
+        // buffers go through the context's state buffers (the loaded state is lost)
+        const spark::Geo& g = ctx->plan.geo;
+        launched(ctx, spark::launch_relayout(g, U_prev, ctx->U[0], 1, ctx->stream), "relayout");
+        if (a != 0.0) launched(ctx, spark::launch_relayout(g, U_n, ctx->U[1], 1, ctx->stream), "relayout");
+        stage_launch(ctx, ctx->U[0], a != 0.0 ? ctx->U[1] : nullptr, a, b, ctx->U[2], false, nullptr, dt, false);
+        launched(ctx, spark::launch_relayout(g, ctx->U[2], U_out, 0, ctx->stream), "relayout");
+        ctx->have_state = false;
     });
 }
 

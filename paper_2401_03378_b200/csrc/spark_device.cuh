@@ -366,6 +366,13 @@ __host__ __device__ __forceinline__ double grav_src(const Geo& g, int v, double 
     return mg;
 }
 
+// Element index of variable 0 of the cell with canonical index q = b*cpb + c
+// (block b, cell c of the block) in the block-interleaved state U[b][v][c].
+__host__ __device__ __forceinline__ long long state_index(const Geo& g, long long q) {
+    const long long b = q / g.cpb;
+    return b * g.bs + (q - b * g.cpb);
+}
+
 // ------------------------------------------------------------ guard gather
 // Conserved values of the cell at sub-box coordinates l (may lie up to ng
 // cells outside the sub-box).  Out-of-box coordinates are resolved per
@@ -424,10 +431,10 @@ __device__ __forceinline__ bool fetch_src(const Geo& g, const double* __restrict
     } else {
         const int bx = l[0] / g.nb[0], by = l[1] / g.nb[1], bz = l[2] / g.nb[2];
         const long long blk = bx + (long long)g.bn[0] * (by + (long long)g.bn[1] * bz);
-        idx = blk * g.cpb + ((long long)(l[2] - bz * g.nb[2]) * g.nb[1] + (l[1] - by * g.nb[1])) * g.nb[0] +
+        idx = blk * g.bs + ((long long)(l[2] - bz * g.nb[2]) * g.nb[1] + (l[1] - by * g.nb[1])) * g.nb[0] +
               (l[0] - bx * g.nb[0]);
         src.p = u + idx;
-        src.vs = g.ncell;
+        src.vs = g.vs;
     }
     src.flip = flip;
     return true;

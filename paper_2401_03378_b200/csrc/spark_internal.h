@@ -32,8 +32,15 @@ struct Geo {
     int off[3];                   // global cell index of the sub-box origin
     int bc[3][2];                 // physical boundary conditions
     int halo[3][2];               // 1: face neighbour is another rank (slab buffer)
-    long long ncell;              // cells of the sub-box (stride between variables)
+    long long ncell;              // cells of the sub-box
     long long cpb;                // cells per block
+    // State layout in HBM: block-interleaved U[b][v][k][j][i],
+    // element (v, block b, cell c of the block) at b*bs + v*vs + c with
+    // vs = cpb, bs = nvar*cpb: one block is one contiguous chunk, so every
+    // variable of a cell is a compile-time offset from one pointer in KB1.
+    // The ABI's canonical layout U[v][b][k][j][i] is converted at set/get.
+    long long vs;                 // stride between variables
+    long long bs;                 // stride between blocks
     long long slab[3];            // cells of one slab of dim d (ng * other extents)
     double dx[3], rdx[3];
     double gamma, cfl;
@@ -68,6 +75,8 @@ cudaError_t launch_stage(const StageArgs& a, int recon, int riemann, cudaStream_
 cudaError_t launch_cfl_min(const Geo& g, const double* u, DevScalars* sc, cudaStream_t s);
 cudaError_t launch_step_begin(DevScalars* sc, double dt_fixed, double t_end, double cfl, cudaStream_t s);
 cudaError_t launch_prim_to_cons(const Geo& g, const double* w, double* u, cudaStream_t s);
+// canonical U[v][b][c] <-> internal U[b][v][c] (to_internal = 1: canonical -> internal)
+cudaError_t launch_relayout(const Geo& g, const double* src, double* dst, int to_internal, cudaStream_t s);
 cudaError_t launch_pack(const Geo& g, const double* u, int dim, int side, double* slab, cudaStream_t s);
 cudaError_t launch_fill_padded(const Geo& g, const double* u, const double* const halo[3][2], double* padded,
                                cudaStream_t s);

@@ -14,7 +14,7 @@
 // formulas).  FP64 throughout: this is a stencil, not a contraction, so there
 // is no tensor-core path.
 //
-// Data layout (HBM): struct-of-arrays block pool U[v][b][k][j][i]; the guard
+// Data layout (HBM): block-interleaved pool U[b][v][k][j][i] (Geo.vs/.bs); the guard
 // cells are NOT stored: each CTA gathers its block's face halos straight from
 // the neighbouring blocks (L2-resident), from the received rank slabs, or from
 // the physical boundary map.
@@ -47,8 +47,9 @@ __global__ void cfl_min_kernel(const Geo g, const double* __restrict__ u, DevSca
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < g.ncell;
          q += (long long)gridDim.x * blockDim.x) {
         double c[NV], w[NV];
+        const long long e = state_index(g, q);
 #pragma unroll
-        for (int v = 0; v < NV; v++) c[v] = u[v * g.ncell + q];
+        for (int v = 0; v < NV; v++) c[v] = u[e + v * g.vs];
         ok &= cons_to_prim<NV>(c, w, g.gamma - 1.0);
         m = fmin(m, cfl_term<NV>(g, w));
     }
@@ -103,16 +104,31 @@ __global__ void prim_to_cons_kernel(const Geo g, const double* __restrict__ w, d
     constexpr int NV = NDIM + 2;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < g.ncell;
          q += (long long)gridDim.x * blockDim.x) {
+        const long long e = state_index(g, q);  // W canonical [v][q], U internal
         const double rho = w[q];
         double u2 = 0.0;
 #pragma unroll
         for (int d = 1; d < NV - 1; d++) {
             const double vel = w[d * g.ncell + q];
             u2 += vel * vel;
-            u[d * g.ncell + q] = rho * vel;
+            u[e + d * g.vs] = rho * vel;
         }
-        u[q] = rho;
-        u[(NV - 1) * g.ncell + q] = w[(NV - 1) * g.ncell + q] / (g.gamma - 1.0) + 0.5 * rho * u2;
+        u[e] = rho;
+        u[e + (NV - 1) * g.vs] = w[(NV - 1) * g.ncell + q] / (g.gamma - 1.0) + 0.5 * rho * u2;
+    }
+}
+
+// canonical U[v][q] (q = b*cpb + c) <-> internal U[b][v][c]; contiguous runs of
+// cpb elements on both sides
+__global__ void relayout_kernel(const Geo g, const double* __restrict__ src, double* __restrict__ dst,
+                                int to_internal) {
+    const long long n = g.ncell * g.nvar;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long v = t / g.ncell, q = t - v * g.ncell;  // canonical element t = v*ncell + q
+        const long long e = state_index(g, q) + v * g.vs;
+        if (to_internal) dst[e] = src[t];
+        else dst[t] = src[e];
     }
 }
 
@@ -205,6 +221,11 @@ cudaError_t launch_prim_to_cons(const Geo& g, const double* w, double* u, cudaSt
     if (g.ndim == 1) prim_to_cons_kernel<1><<<grid, 256, 0, s>>>(g, w, u);
     else if (g.ndim == 2) prim_to_cons_kernel<2><<<grid, 256, 0, s>>>(g, w, u);
     else prim_to_cons_kernel<3><<<grid, 256, 0, s>>>(g, w, u);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_relayout(const Geo& g, const double* src, double* dst, int to_internal, cudaStream_t s) {
+    relayout_kernel<<<grid_for(g.ncell * g.nvar, 256), 256, 0, s>>>(g, src, dst, to_internal);
     return cudaGetLastError();
 }
 

@@ -71,7 +71,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-template <int NDIM, int RECON, int RS, int NBX, int NBY>
+template <int NDIM, int RECON, int RS, int NBX, int NBY, int NBZ>
 __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(const StageArgs A) {
     constexpr bool STAGE_OPS = policy_stage_ops(NDIM, RECON, NBX, NBY);
 #ifdef EXP_NOFC
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
 
     const int nb0 = NBX ? NBX : g.nb[0];
     const int nb1 = NDIM >= 2 ? (NBY ? NBY : g.nb[1]) : 1;
-    const int nb2 = NDIM >= 3 ? g.nb[2] : 1;
+    const int nb2 = NDIM >= 3 ? (NBZ ? NBZ : g.nb[2]) : 1;
     const int P = nb0 * nb1;
     const int tid = threadIdx.x;
     const bool live = tid < P;
@@ -105,9 +105,11 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     const int b = blockIdx.x;
     const int bx = b % g.bn[0], by = (b / g.bn[0]) % g.bn[1], bz = b / (g.bn[0] * g.bn[1]);
     const int cx0 = bx * nb0, cy0 = by * nb1, cz0 = bz * nb2;
-    const long long cpb = (long long)nb0 * nb1 * nb2;
-    const long long bbase = (long long)b * cpb;
-    const long long ncell = g.ncell;
+    // block-interleaved state U[b][v][c]: with a compile-time block shape the
+    // variable stride is an immediate offset from one pointer
+    const long long vs = NBZ ? (long long)NBX * NBY * NBZ : g.vs;
+    const long long bs = NBZ ? (long long)NV * NBX * NBY * NBZ : g.bs;
+    const long long bbase = (long long)b * bs;
     const double* __restrict__ up = A.uprev;
 
     const int cw = nb0 + 2 * NG, ch = NDIM >= 2 ? nb1 + 2 * NG : 1;
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             for (int kk = 0; kk < nb2; kk++) {
                 const long long idx = bbase + ((long long)kk * nb1 + tj) * nb0 + ti;
 #pragma unroll
-                for (int v = 0; v < NV; v++) A.uout[v * ncell + idx] = up[v * ncell + idx];
+                for (int v = 0; v < NV; v++) A.uout[v * vs + idx] = up[v * vs + idx];
             }
         return;
     }
@@ -167,9 +169,9 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
         if (d == 1) { q1 += side ? 1 : -1; inside = q1 >= 0 && q1 < g.bn[1]; }
         if (d == 2) { q2 += side ? 1 : -1; inside = q2 >= 0 && q2 < g.bn[2]; }
         if (d < 0) {
-            ldg_cons<NV>(up + bbase + off, ncell, u);
+            ldg_cons<NV>(up + bbase + off, vs, u);
         } else if (inside) {
-            ldg_cons<NV>(up + (q0 + (long long)g.bn[0] * (q1 + (long long)g.bn[1] * q2)) * cpb + off, ncell, u);
+            ldg_cons<NV>(up + (q0 + (long long)g.bn[0] * (q1 + (long long)g.bn[1] * q2)) * bs + off, vs, u);
         } else {
             fetch_cons<NV>(g, up, A.halo, cx0 + x, cy0 + y, cz0 + z, u);
         }
@@ -293,10 +295,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     // this column: planes z < nb2 of the own block, z >= nb2 of the block above
     // (if inside the sub-box, else the general gather)
     const double* csrc = up + bbase + (long long)tj * nb0 + ti;
-    const double* casrc = (NDIM == 3 && bz + 1 < g.bn[2]) ? csrc + (long long)g.bn[0] * g.bn[1] * cpb : nullptr;
+    const double* casrc = (NDIM == 3 && bz + 1 < g.bn[2]) ? csrc + (long long)g.bn[0] * g.bn[1] * bs : nullptr;
     auto load_col = [&](int z, double* u) {
-        if (z < nb2) ldg_cons<NV>(csrc + (long long)z * P, ncell, u);
-        else if (casrc) ldg_cons<NV>(casrc + (long long)(z - nb2) * P, ncell, u);
+        if (z < nb2) ldg_cons<NV>(csrc + (long long)z * P, vs, u);
+        else if (casrc) ldg_cons<NV>(casrc + (long long)(z - nb2) * P, vs, u);
         else load_cons(ti, tj, z, u);
     };
 
@@ -369,15 +371,15 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             if (STAGE_OPS) {
 #pragma unroll
                 for (int v = 0; v < NV; v++) {
-                    cp_async8(stg + v * P + tid, up + v * ncell + cidx);
-                    if (a != 0.0) cp_async8(stg + (NV + v) * P + tid, A.un + v * ncell + cidx);
+                    cp_async8(stg + v * P + tid, up + v * vs + cidx);
+                    if (a != 0.0) cp_async8(stg + (NV + v) * P + tid, A.un + v * vs + cidx);
                 }
                 cp_async_commit();
             } else {
 #pragma unroll
                 for (int v = 0; v < NV; v++) {
-                    u0v[v] = __ldg(up + v * ncell + cidx);
-                    unv[v] = a != 0.0 ? __ldg(A.un + v * ncell + cidx) : 0.0;
+                    u0v[v] = __ldg(up + v * vs + cidx);
+                    unv[v] = a != 0.0 ? __ldg(A.un + v * vs + cidx) : 0.0;
                 }
             }
         }
@@ -673,7 +675,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 const double u0 = op_u0(v);
                 const double unn = STAGE_OPS ? (a != 0.0 ? stg[(NV + v) * P + tid] : 0.0) : unv[v];
                 const double uo = fma(bco, fma(dt, Lv[v], u0), a * unn);
-                A.uout[v * ncell + idx] = uo;
+                A.uout[v * vs + idx] = uo;
                 un[v] = uo;
                 fzlo[v] = fzhi[v];
             }
@@ -696,10 +698,10 @@ cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <int NDIM, int RECON, int RS, int NBX, int NBY>
+template <int NDIM, int RECON, int RS, int NBX, int NBY, int NBZ>
 cudaError_t launch_t(const StageArgs& a, cudaStream_t s) {
     const size_t smem = stage_smem_bytes(a.g, RECON);
-    auto k = stage_kernel<NDIM, RECON, RS, NBX, NBY>;
+    auto k = stage_kernel<NDIM, RECON, RS, NBX, NBY, NBZ>;
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
     const long long nblk = (long long)a.g.bn[0] * a.g.bn[1] * a.g.bn[2];
@@ -707,11 +709,16 @@ cudaError_t launch_t(const StageArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// Production shapes (16x16 planes) get compile-time block extents.
+// Production shapes (16x16 planes: 16^2 and 16^3 blocks) get compile-time block
+// extents; any other shape runs the runtime-extent kernel.
+bool fast_shape(const Geo& g) {
+    return g.ndim >= 2 && g.nb[0] == 16 && g.nb[1] == 16 && (g.ndim == 2 || g.nb[2] == 16);
+}
+
 template <int NDIM, int RECON, int RS>
 cudaError_t launch_shape(const StageArgs& a, cudaStream_t s) {
-    if (NDIM >= 2 && a.g.nb[0] == 16 && a.g.nb[1] == 16) return launch_t<NDIM, RECON, RS, 16, 16>(a, s);
-    return launch_t<NDIM, RECON, RS, 0, 0>(a, s);
+    if (NDIM >= 2 && fast_shape(a.g)) return launch_t<NDIM, RECON, RS, 16, 16, NDIM == 3 ? 16 : 1>(a, s);
+    return launch_t<NDIM, RECON, RS, 0, 0, 0>(a, s);
 }
 
 template <int NDIM>
@@ -739,7 +746,7 @@ size_t stage_smem_bytes(const Geo& g, int recon) {
     const size_t ring = g.ndim == 3 ? slots * NV * P : 0;
     const size_t cw = nb0 + 2 * NG, ch = g.ndim >= 2 ? nb1 + 2 * NG : 1;
     const size_t cur = NV * cw * ch;
-    const bool k16 = g.ndim >= 2 && nb0 == 16 && nb1 == 16;
+    const bool k16 = fast_shape(g);
 #ifdef EXP_NOFC
     const size_t nst = 2;
 #else

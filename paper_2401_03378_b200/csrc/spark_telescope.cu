@@ -46,8 +46,8 @@ __global__ void __launch_bounds__(kTeleThreads) telescope_kernel(const StageArgs
     const int b = blockIdx.x;
     const int bx = b % g.bn[0], by = (b / g.bn[0]) % g.bn[1];
     const int cx0 = bx * nb0, cy0 = by * nb1;
-    const long long bbase = (long long)b * g.cpb;
-    const long long ncell = g.ncell;
+    const long long bbase = (long long)b * g.bs;  // block-interleaved state U[b][v][c]
+    const long long vs = g.vs;
     const double dt = A.dt_ptr ? *A.dt_ptr : A.dt_value;
     const double gamma = g.gamma, gm1 = g.gamma - 1.0, gm1i = 1.0 / (g.gamma - 1.0);
     const double* const nohalo[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kTeleThreads) telescope_kernel(const StageArgs
     if (A.honor_active && !A.sc->active) {  // t >= t_end: U unchanged
         for (int q = threadIdx.x; q < nb0 * nb1; q += blockDim.x)
 #pragma unroll
-            for (int v = 0; v < NV; v++) A.uout[v * ncell + bbase + q] = A.uprev[v * ncell + bbase + q];
+            for (int v = 0; v < NV; v++) A.uout[v * vs + bbase + q] = A.uprev[v * vs + bbase + q];
         return;
     }
 
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kTeleThreads) telescope_kernel(const StageArgs
             if (s == S) {
                 const long long idx = bbase + (long long)(j - loy) * nb0 + (i - lo);
 #pragma unroll
-                for (int v = 0; v < NV; v++) A.uout[v * ncell + idx] = un[v];
+                for (int v = 0; v < NV; v++) A.uout[v * vs + idx] = un[v];
                 cflmin = fmin(cflmin, cfl_term<NV>(g, w));
             }
         }
