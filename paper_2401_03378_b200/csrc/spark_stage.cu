@@ -45,7 +45,11 @@ constexpr int kThreads = 256;
 // (A 9th "boundary" warp doing all halo work was measured slower in 2-D and
 // 3-D — register cap 112 and a serial boundary critical path — DESIGN.md §4.2.)
 __host__ __device__ constexpr bool policy_stage_ops(int ndim, int recon, int nbx, int nby) {
+#ifdef EXP_NOSTG
+    return false;
+#else
     return nbx == 16 && nby == 16 && ndim == 3 && (recon <= 1 || recon == 3);
+#endif
 }
 // Face-centric x/y reconstruction (16x16 planes, first order / minmod PLM): the
 // thread that solves a face reconstructs both of its states straight from the
@@ -71,8 +75,25 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+// Padded ring (3-D, reconstruction half-width <= 2): the ring slots of the
+// z-march are whole padded planes [NV][(nb1+2NG)][(nb0+2NG)], so the slot of
+// plane k IS the x/y working plane of plane k (its halo cells are written into
+// the slot's padding in S1): no per-plane copy of the column cell into a
+// separate plane (5 LDS + 5 STS per cell and plane).  WENO5's 5 slots would
+// not fit twice per SM; it keeps the compact ring and a separate plane.
+__host__ __device__ constexpr bool policy_pad_ring(int ndim, int recon) {
+#ifdef EXP_NOPADRING
+    return false;
+#else
+    return ndim == 3 && recon != 2 && recon != 4;
+#endif
+}
+
+#ifndef EXP_MINB3D
+#define EXP_MINB3D 2
+#endif
 template <int NDIM, int RECON, int RS, int NBX, int NBY, int NBZ>
-__global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(const StageArgs A) {
+__global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_kernel(const StageArgs A) {
     constexpr bool STAGE_OPS = policy_stage_ops(NDIM, RECON, NBX, NBY);
 #ifdef EXP_NOFC
     constexpr bool FC = false;
@@ -91,6 +112,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     constexpr int R = NG - 1;  // cell-centric reconstruction radius
     constexpr int RS_ = 2 * NG - 1 > 2 ? 2 * NG - 1 : 2;  // ring slots (planes k-R' .. k+NG alive)
     constexpr int RING = NDIM == 3 ? RS_ : 0;
+    constexpr bool PADRING = policy_pad_ring(NDIM, RECON);
     constexpr int RO = NDIM >= 2 ? NG : 0;  // row offset of the interior in cur
     const Geo& g = A.g;
     extern __shared__ double smem[];
@@ -117,9 +139,9 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     const int fxs = nb0 + 1;                   // x faces per row
     const int fxn = fxs * nb1;
     const int fyn = NDIM >= 2 ? nb0 * (nb1 + 1) : 0;
-    double* ring = smem;                       // [RING][NV][P]
-    double* cur = ring + RING * NV * P;        // [NV][CP]
-    double* XA = cur + NV * CP;                // [NV][fxn]: L state at x face, then x flux
+    double* ring = smem;                       // [RING][NV][P] ([RING][NV][CP] if PADRING)
+    double* cur0 = ring + RING * NV * (PADRING ? CP : P);  // [NV][CP] (not with PADRING)
+    double* XA = cur0 + (PADRING ? 0 : NV * CP);  // [NV][fxn]: L state at x face, then x flux
     double* XB = XA + NV * fxn;                // [NV][fxn]: R state at x face (not with FC)
     double* YA = XB + (FC ? 0 : NV * fxn);     // [NV][fyn]
     double* YB = YA + NV * fyn;                // [NV][fyn] (not with FC)
@@ -129,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     constexpr bool HSM = FC && NDIM == 3 && STAGE_OPS;
     double* hs = stg + (STAGE_OPS ? 2 * NV * P : 0);  // [NV][nh]
 #ifdef ABL_NOHALO
-    for (int q = threadIdx.x; q < NV * CP; q += blockDim.x) cur[q] = 1.0;
+    for (int q = threadIdx.x; q < (PADRING ? RING : 1) * NV * CP; q += blockDim.x) (PADRING ? ring : cur0)[q] = 1.0;
     __syncthreads();
 #endif
 
@@ -183,7 +205,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     };
 
     // z machinery (3-D): ring slot of plane z is (z + NG) mod RS_
-    auto ring_at = [&](int z, int v) -> double& { return ring[(((z + NG) % RS_) * NV + v) * P + tid]; };
+    auto ring_at = [&](int z, int v) -> double& {
+        if (PADRING) return ring[(((z + NG) % RS_) * NV + v) * CP + (tj + RO) * cw + ti + NG];
+        return ring[(((z + NG) % RS_) * NV + v) * P + tid];
+    };
     double zhi[NV];   // L state of the face above the current plane (top edge of cell kk)
     double fzlo[NV];  // flux through the face below the current plane
     double fzhi[NV];
@@ -307,6 +332,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     if (NDIM == 3 && live) load_cons(ti, tj, NG, pre);
 
     for (int kk = 0; kk < nb2; kk++) {
+        // the x/y working plane of plane kk (PADRING: its ring slot)
+        double* const cur = PADRING ? ring + ((kk + NG) % RS_) * NV * CP : cur0;
         // ---------------------------------------------------------------- S1
         // No barrier before S1: cur was last read in S3 of the previous plane
         // (fenced by the S3->S4 barrier) and the face arrays written in S2 are
@@ -318,13 +345,15 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 if (kk + 1 < nb2) load_col(kk + 1 + NG, pre);  // prefetch the next plane
 #pragma unroll
                 for (int v = 0; v < NV; v++) ring_at(kk + NG, v) = w[v];
+                if (!PADRING) {
 #pragma unroll
-                for (int v = 0; v < NV; v++) w[v] = ring_at(kk, v);
+                    for (int v = 0; v < NV; v++) cur[v * CP + (tj + RO) * cw + ti + NG] = ring_at(kk, v);
+                }
             } else {
                 load_prim(ti, tj, kk, w);
-            }
 #pragma unroll
-            for (int v = 0; v < NV; v++) cur[v * CP + (tj + RO) * cw + ti + NG] = w[v];
+                for (int v = 0; v < NV; v++) cur[v * CP + (tj + RO) * cw + ti + NG] = w[v];
+            }
         }
         if (HPF) {  // one halo cell per thread, prefetched one plane ahead
             if (hact) {
@@ -689,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     if (!ok) atomicOr(&A.sc->status, 1);
     if (A.last) {
         __syncthreads();
-        block_min_to(cflmin, cur, &A.sc->acc);  // cur is dead here
+        block_min_to(cflmin, smem, &A.sc->acc);  // the planes are dead here
     }
 }
 
@@ -743,9 +772,10 @@ size_t stage_smem_bytes(const Geo& g, int recon) {
     const int nb0 = g.nb[0], nb1 = g.ndim >= 2 ? g.nb[1] : 1;
     const size_t P = (size_t)nb0 * nb1;
     const size_t slots = 2 * NG - 1 > 2 ? 2 * NG - 1 : 2;
-    const size_t ring = g.ndim == 3 ? slots * NV * P : 0;
     const size_t cw = nb0 + 2 * NG, ch = g.ndim >= 2 ? nb1 + 2 * NG : 1;
-    const size_t cur = NV * cw * ch;
+    const bool pad = policy_pad_ring(g.ndim, recon);
+    const size_t ring = g.ndim == 3 ? slots * NV * (pad ? cw * ch : P) : 0;
+    const size_t cur = pad ? 0 : NV * cw * ch;
     const bool k16 = fast_shape(g);
 #ifdef EXP_NOFC
     const size_t nst = 2;
