@@ -280,11 +280,22 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     // 16x16 planes: nh <= 256, so thread h owns halo cell h for every plane and
     // prefetches it one plane ahead (raw conserved values in registers)
     constexpr bool HPF = NBX == 16 && NBY == 16;
+    // HLATE (3-D face-centric PLM / first order with the padded ring): the halo
+    // cells of plane k+1 are converted and written into the padding of plane
+    // k+1's ring slot during S2/S3 of plane k by the LAST nh threads (warps 4-7),
+    // which wait there for warp 0's block-boundary faces anyway; S1 then has no
+    // halo work and the S1->S2 barrier no imbalance.
+#ifdef EXP_NOHLATE
+    constexpr bool HLATE = false;
+#else
+    constexpr bool HLATE = HSM && PADRING;
+#endif
 #ifdef ABL_NOHALO
     const bool hact = false;
 #else
-    const bool hact = HPF && tid < nh;
+    const bool hact = HPF && (HLATE ? tid >= P - nh : tid < nh);
 #endif
+    const int hid = HLATE ? tid - (P - nh) : tid;  // halo cell of this thread
     int hcx = 0, hcy = 0;
     double hpre[NV];
     // Per-plane sources resolved once: a halo cell in a face-neighbour block of
@@ -297,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     const double* hp = up;
     int hvs = 0, hzf = 0;
     if (hact) {
-        halo_cell(tid, hcx, hcy);
+        halo_cell(hid, hcx, hcy);
         if (NDIM == 3) {
             Src s0, s1;
             fetch_src(g, up, A.halo, cx0 + hcx, cy0 + hcy, cz0, s0);
@@ -305,7 +316,19 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
             hp = s0.p;
             hvs = (int)s0.vs;
             hzf = (int)((s1.p - s0.p) * 16) | s0.flip;
-            if (HSM) {
+            if (HLATE) {  // plane 0 now (into its slot's padding), plane 1 in flight
+                double w[NV];
+                load_src<NV>(hp, hvs, s0.flip, hpre);
+                ok &= cons_to_prim<NV>(hpre, w, gm1);
+#pragma unroll
+                for (int v = 0; v < NV; v++) ring[((NG % RS_) * NV + v) * CP + (hcy + RO) * cw + hcx + NG] = w[v];
+                if (nb2 > 1) {
+                    const double* src = hp + (hzf >> 4);
+#pragma unroll
+                    for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + hid, src + (long long)v * hvs);
+                    cp_async_commit();
+                }
+            } else if (HSM) {
 #pragma unroll
                 for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + tid, hp + (long long)v * hvs);
                 cp_async_commit();
@@ -355,7 +378,9 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                 for (int v = 0; v < NV; v++) cur[v * CP + (tj + RO) * cw + ti + NG] = w[v];
             }
         }
-        if (HPF) {  // one halo cell per thread, prefetched one plane ahead
+        if (HLATE) {
+            // halo of this plane already in its slot (written during plane kk-1)
+        } else if (HPF) {  // one halo cell per thread, prefetched one plane ahead
             if (hact) {
                 double w[NV];
                 if (HSM) {
@@ -674,6 +699,26 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     if (q < nb1) xface(q, 0);
                     else yface(q - nb1, 0);
                 }
+            }
+        }
+        if (HLATE && hact && kk + 1 < nb2) {  // halo of plane kk+1 -> its slot
+            double w[NV];
+            cp_async_wait_all();
+#pragma unroll
+            for (int v = 0; v < NV; v++) hpre[v] = hs[v * nh + hid];
+#pragma unroll
+            for (int d = 0; d < NV - 2; d++)  // reflecting-boundary image: momentum sign
+                hpre[1 + d] = __hiloint2double(__double2hiint(hpre[1 + d]) ^ (((hzf >> (1 + d)) & 1) << 31),
+                                               __double2loint(hpre[1 + d]));
+            ok &= cons_to_prim<NV>(hpre, w, gm1);
+            double* nxt = ring + ((kk + 1 + NG) % RS_) * NV * CP + (hcy + RO) * cw + hcx + NG;
+#pragma unroll
+            for (int v = 0; v < NV; v++) nxt[v * CP] = w[v];
+            if (kk + 2 < nb2) {
+                const double* src = hp + (long long)(kk + 2) * (hzf >> 4);
+#pragma unroll
+                for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + hid, src + (long long)v * hvs);
+                cp_async_commit();
             }
         }
         __syncthreads();
