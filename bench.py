@@ -118,7 +118,7 @@ class ClockSampler:
             for bit, name in self.REASONS.items():
                 if r & bit:
                     self.reasons.add(name)
-            if self._stop.wait(0.01):
+            if self._stop.wait(0.005):
                 break
 
     def __enter__(self):
@@ -148,7 +148,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [f"nvml unavailable: {self.err}"],
                     "samples": 0}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml 10 ms"}
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml 5 ms"}
 
 
 RECONS = {"first": 0, "plm": 1, "weno5": 2, "mc": 3, "wenoz": 4}
@@ -229,7 +229,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)  # >= 0.17 s timed: enough NVML clock samples
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c4_sedov3d_plm", choices=sorted(si.PRESETS))
     ap.add_argument("--graphs", action="store_true",

@@ -118,17 +118,25 @@ __global__ void prim_to_cons_kernel(const Geo g, const double* __restrict__ w, d
     }
 }
 
-// canonical U[v][q] (q = b*cpb + c) <-> internal U[b][v][c]; contiguous runs of
-// cpb elements on both sides
+// canonical U[v][q] (q = b*cpb + c) <-> internal U[b][v][c]: one CTA per
+// (variable, block) chunk of cpb contiguous elements on both sides (16-byte
+// accesses when cpb is even); no index division per element
 __global__ void relayout_kernel(const Geo g, const double* __restrict__ src, double* __restrict__ dst,
                                 int to_internal) {
-    const long long n = g.ncell * g.nvar;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
-         t += (long long)gridDim.x * blockDim.x) {
-        const long long v = t / g.ncell, q = t - v * g.ncell;  // canonical element t = v*ncell + q
-        const long long e = state_index(g, q) + v * g.vs;
-        if (to_internal) dst[e] = src[t];
-        else dst[t] = src[e];
+    const long long nblk = g.ncell / g.cpb, nchunk = nblk * g.nvar;
+    const bool vec = (g.cpb & 1) == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    for (long long ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
+        const long long v = ch / nblk, b = ch - v * nblk;
+        const long long canon = v * g.ncell + b * g.cpb, inter = b * g.bs + v * g.vs;
+        const double* s = src + (to_internal ? canon : inter);
+        double* d = dst + (to_internal ? inter : canon);
+        if (vec) {
+            const double2* s2 = reinterpret_cast<const double2*>(s);
+            double2* d2 = reinterpret_cast<double2*>(d);
+            for (long long c = threadIdx.x; c < g.cpb / 2; c += blockDim.x) d2[c] = __ldcs(s2 + c);
+        } else {
+            for (long long c = threadIdx.x; c < g.cpb; c += blockDim.x) d[c] = __ldcs(s + c);
+        }
     }
 }
 
@@ -225,7 +233,8 @@ cudaError_t launch_prim_to_cons(const Geo& g, const double* w, double* u, cudaSt
 }
 
 cudaError_t launch_relayout(const Geo& g, const double* src, double* dst, int to_internal, cudaStream_t s) {
-    relayout_kernel<<<grid_for(g.ncell * g.nvar, 256), 256, 0, s>>>(g, src, dst, to_internal);
+    const long long nchunk = g.ncell / g.cpb * g.nvar;
+    relayout_kernel<<<(unsigned)(nchunk < 148LL * 64 ? nchunk : 148LL * 64), 256, 0, s>>>(g, src, dst, to_internal);
     return cudaGetLastError();
 }
 

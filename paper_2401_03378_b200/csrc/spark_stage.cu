@@ -74,6 +74,8 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+// all but the most recent commit group complete
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 // Padded ring (3-D, reconstruction half-width <= 2): the ring slots of the
 // z-march are whole padded planes [NV][(nb1+2NG)][(nb0+2NG)], so the slot of
@@ -722,7 +724,9 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
         }
         if (HLATE && hact && kk + 1 < nb2) {  // halo of plane kk+1 -> its slot
             double w[NV];
-            cp_async_wait_all();
+            // pending: halo(kk+1) (committed during plane kk-1), then this
+            // plane's S4 operands: wait for the halo only
+            cp_async_wait_1();
 #pragma unroll
             for (int v = 0; v < NV; v++) hpre[v] = hs[v * nh + hid];
 #pragma unroll
@@ -756,7 +760,12 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     else Lv[v] = -(dfx + dfy) - (fzhi[v] - fzlo[v]) * g.rdx[2];
                 }
             }
-            if (STAGE_OPS) cp_async_wait_all();
+            if (STAGE_OPS) {
+                // HLATE halo threads leave the halo of plane kk+2 (committed
+                // last) in flight; everything else waits for the operands
+                if (HLATE && hact && kk + 2 < nb2) cp_async_wait_1();
+                else cp_async_wait_all();
+            }
             auto op_u0 = [&](int v) { return STAGE_OPS ? stg[v * P + tid] : u0v[v]; };
             if (g.has_grav) {  // grvAccel source at U^(s-1) (CTA-uniform branch)
                 double grho = 0.0, gmg = 0.0;

@@ -27,7 +27,7 @@ def summarise(rep):
                 except ValueError:
                     continue
                 scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "msecond": 1e-3, "usecond": 1e-6,
-                         "nsecond": 1e-9, "second": 1}.get(u, None)
+                         "nsecond": 1e-9, "second": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1}.get(u, None)
                 d[h] = x * scale if scale else x
         d["kernel"] = [v for h, v in zip(hdr, row) if h == "Kernel Name"][0][:80]
         res.append(d)
