@@ -115,6 +115,12 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     constexpr int RS_ = 2 * NG - 1 > 2 ? 2 * NG - 1 : 2;  // ring slots (planes k-R' .. k+NG alive)
     constexpr int RING = NDIM == 3 ? RS_ : 0;
     constexpr bool PADRING = policy_pad_ring(NDIM, RECON);
+    // own x / y face fluxes kept in registers for S4 (face-centric 16x16 path)
+#ifdef EXP_NO_OWNF
+    constexpr bool OWNF = false;
+#else
+    constexpr bool OWNF = FC && !FUSE && NBX == 16 && NBY == 16 && NDIM >= 2;  // +0.5 %
+#endif
 #ifdef EXP_ZTOP_ALL
     constexpr bool ZTOP = true;
 #else
@@ -511,8 +517,9 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
         if (!FC) __syncthreads();
         // ---------------------------------------------------------------- S3
         // x face at column f of row r: cells (f-1, f); y face at row f of column r
-        auto xface = [&](int r, int f) {
-            double wl[NV], wr[NV], fl[NV];
+        double fxo[NV], fyo[NV];  // this thread's own x / y face fluxes (OWNF)
+        auto xface = [&](int r, int f, double* fl) {
+            double wl[NV], wr[NV];
 #pragma unroll
             for (int v = 0; v < NV; v++) {
                 if (FC) {
@@ -534,8 +541,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
 #pragma unroll
             for (int v = 0; v < NV; v++) XA[v * fxn + r * fxs + f] = fl[v];
         };
-        auto yface = [&](int r, int f) {
-            double wl[NV], wr[NV], fl[NV];
+        auto yface = [&](int r, int f, double* fl) {
+            double wl[NV], wr[NV];
 #pragma unroll
             for (int v = 0; v < NV; v++) {
                 if (FC) {
@@ -668,8 +675,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
             }
         } else {
             if (live) {
-                xface(tj, ti + 1);
-                if (NDIM >= 2) yface(ti, tj + 1);
+                xface(tj, ti + 1, fxo);
+                if (NDIM >= 2) yface(ti, tj + 1, fyo);
                 if (NDIM == 3) {
                     zflux(kk, zhi, zlo, fzhi);
 #pragma unroll
@@ -717,8 +724,9 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                 }
             } else {
                 for (int q = tid; q < nbf; q += blockDim.x) {
-                    if (q < nb1) xface(q, 0);
-                    else yface(q - nb1, 0);
+                    double scr[NV];
+                    if (q < nb1) xface(q, 0, scr);
+                    else yface(q - nb1, 0, scr);
                 }
             }
         }
@@ -751,11 +759,13 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
             double un[NV], Lv[NV];
 #pragma unroll
             for (int v = 0; v < NV; v++) {
-                const double dfx = (XA[v * fxn + tj * fxs + ti + 1] - XA[v * fxn + tj * fxs + ti]) * g.rdx[0];
+                const double fxp = OWNF ? fxo[v] : XA[v * fxn + tj * fxs + ti + 1];
+                const double dfx = (fxp - XA[v * fxn + tj * fxs + ti]) * g.rdx[0];
                 if (NDIM == 1) {
                     Lv[v] = -dfx;
                 } else {
-                    const double dfy = (YA[v * fyn + (tj + 1) * nb0 + ti] - YA[v * fyn + tj * nb0 + ti]) * g.rdx[1];
+                    const double fyp = OWNF ? fyo[v] : YA[v * fyn + (tj + 1) * nb0 + ti];
+                    const double dfy = (fyp - YA[v * fyn + tj * nb0 + ti]) * g.rdx[1];
                     if (NDIM == 2) Lv[v] = -(dfx + dfy);
                     else Lv[v] = -(dfx + dfy) - (fzhi[v] - fzlo[v]) * g.rdx[2];
                 }
