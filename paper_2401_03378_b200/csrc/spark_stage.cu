@@ -74,8 +74,6 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-// all but the most recent commit group complete
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 // Padded ring (3-D, reconstruction half-width <= 2): the ring slots of the
 // z-march are whole padded planes [NV][(nb1+2NG)][(nb0+2NG)], so the slot of
@@ -306,9 +304,11 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     constexpr bool HPF = NBX == 16 && NBY == 16;
     // HLATE (3-D face-centric PLM / first order with the padded ring): the halo
     // cells of plane k+1 are converted and written into the padding of plane
-    // k+1's ring slot during S2/S3 of plane k by the LAST nh threads (warps 4-7),
-    // which wait there for warp 0's block-boundary faces anyway; S1 then has no
-    // halo work and the S1->S2 barrier no imbalance.
+    // k+1's ring slot at the start of S2 of plane k by the LAST nh threads
+    // (warps 4-7, which have one face solve less than warp 0 per plane), so S1
+    // has no halo work and the S1->S2 barrier no imbalance.  The cp.async of
+    // that halo was issued one plane earlier and completed by the previous S4's
+    // wait (measured: start of S2 +3.6 % over end of S3).
 #ifdef EXP_NOHLATE
     constexpr bool HLATE = false;
 #else
@@ -445,6 +445,26 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
         }
         __syncthreads();
         // ---------------------------------------------------------------- S2
+        if (HLATE && hact && kk + 1 < nb2) {  // halo of plane kk+1 -> its slot
+            double w[NV];
+            cp_async_wait_all();  // no-op: complete since S4 of the previous plane
+#pragma unroll
+            for (int v = 0; v < NV; v++) hpre[v] = hs[v * nh + hid];
+#pragma unroll
+            for (int d = 0; d < NV - 2; d++)  // reflecting-boundary image: momentum sign
+                hpre[1 + d] = __hiloint2double(__double2hiint(hpre[1 + d]) ^ (((hzf >> (1 + d)) & 1) << 31),
+                                               __double2loint(hpre[1 + d]));
+            ok &= cons_to_prim<NV>(hpre, w, gm1);
+            double* nxt = ring + ((kk + 1 + NG) % RS_) * NV * CP + (hcy + RO) * cw + hcx + NG;
+#pragma unroll
+            for (int v = 0; v < NV; v++) nxt[v * CP] = w[v];
+            if (kk + 2 < nb2) {
+                const double* src = hp + (long long)(kk + 2) * (hzf >> 4);
+#pragma unroll
+                for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + hid, src + (long long)v * hvs);
+                cp_async_commit();
+            }
+        }
         // operands of the S4 update, requested now so the loads overlap S2/S3
         double u0v[NV], unv[NV];
         const long long cidx = bbase + ((long long)kk * nb1 + tj) * nb0 + ti;
@@ -686,7 +706,11 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
             if (FC && NBX == 16 && NBY == 16) {
                 // warp 0: the 32 block-boundary faces in one pass (y faces in the
                 // x frame with u_x <-> u_y swapped, bitwise identical; see FUSE)
+#ifdef ABL_NOBND
+                if (false) {
+#else
                 if (tid < 32) {
+#endif
                     const bool isy = tid >= 16;
                     const int q = tid & 15;
                     double bl[NV], br[NV], fb[NV];
@@ -730,28 +754,6 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                 }
             }
         }
-        if (HLATE && hact && kk + 1 < nb2) {  // halo of plane kk+1 -> its slot
-            double w[NV];
-            // pending: halo(kk+1) (committed during plane kk-1), then this
-            // plane's S4 operands: wait for the halo only
-            cp_async_wait_1();
-#pragma unroll
-            for (int v = 0; v < NV; v++) hpre[v] = hs[v * nh + hid];
-#pragma unroll
-            for (int d = 0; d < NV - 2; d++)  // reflecting-boundary image: momentum sign
-                hpre[1 + d] = __hiloint2double(__double2hiint(hpre[1 + d]) ^ (((hzf >> (1 + d)) & 1) << 31),
-                                               __double2loint(hpre[1 + d]));
-            ok &= cons_to_prim<NV>(hpre, w, gm1);
-            double* nxt = ring + ((kk + 1 + NG) % RS_) * NV * CP + (hcy + RO) * cw + hcx + NG;
-#pragma unroll
-            for (int v = 0; v < NV; v++) nxt[v * CP] = w[v];
-            if (kk + 2 < nb2) {
-                const double* src = hp + (long long)(kk + 2) * (hzf >> 4);
-#pragma unroll
-                for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + hid, src + (long long)v * hvs);
-                cp_async_commit();
-            }
-        }
         __syncthreads();
         // ---------------------------------------------------------------- S4
         if (live) {
@@ -770,12 +772,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     else Lv[v] = -(dfx + dfy) - (fzhi[v] - fzlo[v]) * g.rdx[2];
                 }
             }
-            if (STAGE_OPS) {
-                // HLATE halo threads leave the halo of plane kk+2 (committed
-                // last) in flight; everything else waits for the operands
-                if (HLATE && hact && kk + 2 < nb2) cp_async_wait_1();
-                else cp_async_wait_all();
-            }
+            if (STAGE_OPS) cp_async_wait_all();  // operands (and, HLATE, the next halo)
             auto op_u0 = [&](int v) { return STAGE_OPS ? stg[v * P + tid] : u0v[v]; };
             if (g.has_grav) {  // grvAccel source at U^(s-1) (CTA-uniform branch)
                 double grho = 0.0, gmg = 0.0;
