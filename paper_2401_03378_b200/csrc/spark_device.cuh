@@ -212,9 +212,9 @@ __host__ __device__ __forceinline__ void recon_cell(const double* s, double& lo,
         const double t0 = fma(-2.0, b, a) + c, u0 = fma(3.0, c, fma(-4.0, b, a));
         const double t1 = fma(-2.0, c, b) + d, u1 = b - d;
         const double t2 = fma(-2.0, d, c) + e, u2 = fma(3.0, c, fma(-4.0, d, e));
-        const double e0 = eps4 + fma(k13 * t0, t0, u0 * u0);
-        const double e1 = eps4 + fma(k13 * t1, t1, u1 * u1);
-        const double e2 = eps4 + fma(k13 * t2, t2, u2 * u2);
+        const double e0 = fma(k13 * t0, t0, fma(u0, u0, eps4));  // eps folded: one op fewer
+        const double e1 = fma(k13 * t1, t1, fma(u1, u1, eps4));
+        const double e2 = fma(k13 * t2, t2, fma(u2, u2, eps4));
         const double s0 = e0 * e0, s1 = e1 * e1, s2 = e2 * e2;
         const double P0 = s1 * s2, P1 = 6.0 * (s0 * s2), P2 = s0 * s1;
         // right edge (i+1/2): stencils (a,b,c), (b,c,d), (c,d,e), weights 1 : 6 : 3
