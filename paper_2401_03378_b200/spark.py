@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libspark.so")
+LIB_PATH = os.environ.get("SPARK_LIB") or os.path.join(_PKG, "lib", "libspark.so")  # SPARK_LIB: design-experiment builds
 
 SPARK_OK, SPARK_ERR_ARG, SPARK_ERR_CUDA, SPARK_ERR_NCCL, SPARK_ERR_OOM, SPARK_ERR_NONPHYSICAL, SPARK_ERR_STATE = range(7)
 
