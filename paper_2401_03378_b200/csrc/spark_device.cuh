@@ -468,14 +468,21 @@ __device__ __forceinline__ double warp_min(double x) {
     return x;
 }
 
-// CFL term of one primitive state: min_d dx_d / (|u_d| + c)  (reading R7).
+// CFL term of one primitive state: min_d dx_d / (|u_d| + c)  (reading R7),
+// evaluated as 1 / max_d (|u_d| + c) / dx_d (one reciprocal instead of ndim)
+// with c = gamma p / sqrt(gamma p rho) (no reciprocal of rho); every GPU path
+// uses this function, so the CFL minimum stays bitwise rank-invariant.
 template <int NV>
 __device__ __forceinline__ double cfl_term(const Geo& g, const double* w) {
-    const double c = sqrt_fast(g.gamma * w[NV - 1] * rcp(w[0]));
-    double best = INFINITY;
+    const double gp = g.gamma * w[NV - 1];
+    const double c = gp * rsqrt_fast(gp * w[0]);
+    double m = (fabs(w[1]) + c) * g.rdx[0];
 #pragma unroll
-    for (int d = 0; d < NV - 2; d++) best = fmin(best, g.dx[d] * rcp(fabs(w[1 + d]) + c));
-    return best;
+    for (int d = 1; d < NV - 2; d++) {
+        const double x = (fabs(w[1 + d]) + c) * g.rdx[d];
+        m = x > m ? x : m;
+    }
+    return rcp(m);
 }
 
 // Block-wide min of x -> atomicMin on the u64 bits (positive doubles order
