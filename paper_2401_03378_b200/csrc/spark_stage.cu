@@ -113,6 +113,15 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     constexpr int RS_ = 2 * NG - 1 > 2 ? 2 * NG - 1 : 2;  // ring slots (planes k-R' .. k+NG alive)
     constexpr int RING = NDIM == 3 ? RS_ : 0;
     constexpr bool PADRING = policy_pad_ring(NDIM, RECON);
+    // 3-D without staged operands (WENO5): the S4 operands are only prefetched
+    // into L2 in S2 and loaded in S4, so no 20 registers are held across S3
+    // (spills 148 -> 44 B; WENO5 8.6 -> 8.9 G zone-updates/s; 2-D measured 3 %
+    // slower that way and keeps the register prefetch)
+#ifdef EXP_NO_L2PF
+    constexpr bool L2PF = false;
+#else
+    constexpr bool L2PF = !STAGE_OPS && NDIM == 3;
+#endif
     // own x / y face fluxes kept in registers for S4 (face-centric 16x16 path)
 #ifdef EXP_NO_OWNF
     constexpr bool OWNF = false;
@@ -476,6 +485,12 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     if (a != 0.0) cp_async8(stg + (NV + v) * P + tid, A.un + v * vs + cidx);
                 }
                 cp_async_commit();
+            } else if (L2PF) {  // only an L2 prefetch now; loaded in S4 (no registers held)
+#pragma unroll
+                for (int v = 0; v < NV; v++) {
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(up + v * vs + cidx));
+                    if (a != 0.0) asm volatile("prefetch.global.L2 [%0];" ::"l"(A.un + v * vs + cidx));
+                }
             } else {
 #pragma unroll
                 for (int v = 0; v < NV; v++) {
@@ -780,6 +795,13 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                 }
             }
             if (STAGE_OPS) cp_async_wait_all();  // operands (and, HLATE, the next halo)
+            if (L2PF) {
+#pragma unroll
+                for (int v = 0; v < NV; v++) {
+                    u0v[v] = __ldg(up + v * vs + cidx);
+                    unv[v] = a != 0.0 ? __ldg(A.un + v * vs + cidx) : 0.0;
+                }
+            }
             auto op_u0 = [&](int v) { return STAGE_OPS ? stg[v * P + tid] : u0v[v]; };
             if (g.has_grav) {  // grvAccel source at U^(s-1) (CTA-uniform branch)
                 double grho = 0.0, gmg = 0.0;
