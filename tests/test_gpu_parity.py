@@ -67,6 +67,12 @@ STAGE_CASES = [
     si.Problem("3d_weno_hllc", 3, (16, 16, 16), (2, 1, 2), 3, 2, 1, 3, 0.3, bc=((0, 0), (1, 2), (1, 1))),
     si.Problem("3d_weno_hll_odd", 3, (6, 5, 7), (3, 2, 2), 3, 2, 0, 3, 0.3, bc=((2, 1), (0, 0), (0, 0))),
     si.Problem("3d_first_hllc", 3, (4, 4, 4), (2, 3, 2), 1, 0, 1, 2, 0.3, bc=((1, 1),) * 3),
+    # production 16^3 kernels: face-centric first order (halo on warps 6-7) with
+    # reflecting y faces, PLM with reflecting x/y faces and RK3 (halo sign flips
+    # in the in-S2 halo conversion), and 16x16x8 blocks (runtime-extent kernel)
+    si.Problem("3d_first16_hll_refl", 3, (16, 16, 16), (2, 1, 2), 1, 0, 0, 2, 0.3, bc=((1, 1), (2, 2), (0, 0))),
+    si.Problem("3d_plm16_hll_reflxy", 3, (16, 16, 16), (1, 2, 2), 2, 1, 0, 3, 0.3, bc=((2, 2), (2, 1), (1, 1))),
+    si.Problem("3d_plm_16x16x8", 3, (16, 16, 8), (2, 2, 2), 2, 1, 1, 2, 0.3, bc=((0, 0), (1, 1), (2, 1))),
 ]
 
 
