@@ -44,11 +44,14 @@ constexpr int kThreads = 256;
 //   does not and prefetches into registers).
 // (A 9th "boundary" warp doing all halo work was measured slower in 2-D and
 // 3-D — register cap 112 and a serial boundary critical path — DESIGN.md §4.2.)
+//   Superseded by the L2 prefetch of the operands (L2PF below): without the
+//   20 KiB staging buffer a 3-D PLM CTA needs 76 instead of 96 KiB of shared
+//   memory, which leaves the SM a larger L1 (+1 %); kept as an experiment.
 __host__ __device__ constexpr bool policy_stage_ops(int ndim, int recon, int nbx, int nby) {
-#ifdef EXP_NOSTG
-    return false;
-#else
+#ifdef EXP_STG
     return nbx == 16 && nby == 16 && ndim == 3 && (recon <= 1 || recon == 3);
+#else
+    return false;
 #endif
 }
 // Face-centric x/y reconstruction (16x16 planes, first order / minmod PLM): the
@@ -113,10 +116,11 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     constexpr int RS_ = 2 * NG - 1 > 2 ? 2 * NG - 1 : 2;  // ring slots (planes k-R' .. k+NG alive)
     constexpr int RING = NDIM == 3 ? RS_ : 0;
     constexpr bool PADRING = policy_pad_ring(NDIM, RECON);
-    // 3-D without staged operands (WENO5): the S4 operands are only prefetched
-    // into L2 in S2 and loaded in S4, so no 20 registers are held across S3
-    // (spills 148 -> 44 B; WENO5 8.6 -> 8.9 G zone-updates/s; 2-D measured 3 %
-    // slower that way and keeps the register prefetch)
+    // 3-D: the S4 operands are only prefetched into L2 in S2 and loaded in S4,
+    // so no 20 registers are held across S3 (WENO5 spills 148 -> 44 B, 8.6 ->
+    // 8.9 G zone-updates/s) and no shared-memory staging is needed (PLM +1 %
+    // over cp.async staging); 2-D measured 3 % slower that way and keeps the
+    // register prefetch
 #ifdef EXP_NO_L2PF
     constexpr bool L2PF = false;
 #else
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     double* stg = YB + (FC ? 0 : NV * fyn);    // [2][NV][P] staged S4 operands (STAGE_OPS)
     // FC in 3-D: the next plane's raw halo cells arrive by cp.async in shared
     // memory (no prefetch registers held across the plane)
-    constexpr bool HSM = FC && NDIM == 3 && STAGE_OPS;
+    constexpr bool HSM = FC && NDIM == 3;
     double* hs = stg + (STAGE_OPS ? 2 * NV * P : 0);  // [NV][nh]
 #ifdef ABL_NOHALO
     for (int q = threadIdx.x; q < (PADRING ? RING : 1) * NV * CP; q += blockDim.x) (PADRING ? ring : cur0)[q] = 1.0;
@@ -895,7 +899,7 @@ size_t stage_smem_bytes(const Geo& g, int recon) {
     const size_t fy = g.ndim >= 2 ? nst * NV * (size_t)nb0 * (nb1 + 1) : 0;
     const size_t stg = k16 && policy_stage_ops(g.ndim, recon, 16, 16) ? 2 * NV * P : 0;
     const size_t nh = 2 * (size_t)NG * (nb0 + nb1);
-    const size_t hsm = k16 && g.ndim == 3 && nst == 1 && stg ? NV * nh : 0;  // HSM staging
+    const size_t hsm = k16 && g.ndim == 3 && nst == 1 ? NV * nh : 0;  // HSM staging
     return (ring + cur + fx + fy + stg + hsm) * sizeof(double);
 }
 
