@@ -69,7 +69,8 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        _lib = ctypes.CDLL(build())
+        # SPARK_ORACLE_LIB: a mutated copy of the oracle (tools/oracle_mutations.py)
+        _lib = ctypes.CDLL(os.environ.get("SPARK_ORACLE_LIB") or build())
         P = ctypes.POINTER
         d, i32, i64 = ctypes.c_double, ctypes.c_int, ctypes.c_long
         dp = P(ctypes.c_double)
