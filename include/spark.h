@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SPARK_ABI_VERSION 2
+#define SPARK_ABI_VERSION 3
 
 typedef enum {
     SPARK_OK = 0,
@@ -106,7 +106,8 @@ const char* spark_status_string(spark_status st);
 
 /* Validate a configuration for nranks ranks.  Checks ndim, nb >= ng, ng large
  * enough for recon, rk_stages, gamma > 1, cfl > 0, the block grid divisible
- * by the process grid, and nb[0]*nb[1] <= 1024 (one CTA thread per column). */
+ * by the process grid, and nb[0]*nb[1] <= 256 (one thread per column of a
+ * 256-thread CTA). */
 spark_status spark_check_config(const spark_config* cfg, int32_t nranks);
 
 /* Process grid (P_x, P_y, P_z) used for nranks ranks: the factorisation of
@@ -180,6 +181,12 @@ spark_status spark_set_primitive(spark_ctx* ctx, const double* W, int32_t on_dev
  * reports a non-physical state. */
 spark_status spark_get_state(spark_ctx* ctx, double* U, int32_t on_device);
 
+/* Restore the simulation time and step count (checkpoint/resume: load the
+ * saved U with spark_set_state, which resets t = 0 and steps = 0, then call
+ * this with the saved values).  The next step then continues bitwise as the
+ * uninterrupted run would (dt comes from U, the clip from t).  Asynchronous. */
+spark_status spark_set_time(spark_ctx* ctx, double t, int64_t steps);
+
 /* Time, completed steps and dt of the last step.  Synchronises. */
 spark_status spark_get_time(spark_ctx* ctx, double* t, int64_t* steps, double* dt_last);
 
@@ -203,8 +210,16 @@ spark_status spark_fill_guardcells(spark_ctx* ctx, double* padded_out);
  * dt <= 0: CFL dt of U^n (cfl * global min), clipped to t_end - t when
  * t_end > 0; once t >= t_end*(1 - 1e-14) further steps leave U unchanged.
  * dt_used == NULL: fully asynchronous.  dt_used != NULL: synchronises, writes
- * the dt taken and checks the status word; on SPARK_ERR_NONPHYSICAL the state
- * is rolled back to U^n of this step. */
+ * the dt taken and checks the failure word.
+ * Errors are rank-consistent: a stage that produces rho <= 0, p <= 0 or NaN
+ * records the step number in the failure word, which is min-reduced over all
+ * ranks together with the CFL minimum (one collective per step), so every rank
+ * sees the same decision.  SPARK_ERR_NONPHYSICAL then either (a) the failing
+ * step is the one this call executed: every rank's state is rolled back to
+ * U^n, t and the step count of that step; or (b) it was an earlier step
+ * enqueued without a check: all steps after it were frozen (no time advance)
+ * on every rank and nothing is rolled back; spark_last_error names the step.
+ * Collective with nranks > 1: every rank must pass dt_used alike. */
 spark_status spark_step(spark_ctx* ctx, double dt, double t_end, double* dt_used);
 
 /* nsteps steps of spark_step (same dt / t_end semantics), fully asynchronous.
@@ -231,7 +246,9 @@ spark_status spark_advance(spark_ctx* ctx, int64_t max_steps, double t_end, int3
                            int64_t* steps_done);
 
 /* spark_step for the contexts of one spark_init_local_group, stage by stage
- * in lockstep (exchange between virtual ranks, global dt minimum). */
+ * in lockstep (exchange between virtual ranks, global dt minimum and failure
+ * word).  With dt_used != NULL a failure rolls back ALL members (or, for an
+ * earlier unchecked step, none) before SPARK_ERR_NONPHYSICAL is returned. */
 spark_status spark_step_group(spark_ctx* const* ctxs, int32_t n, double dt, double t_end, double* dt_used);
 
 /* Apply ONE fused stage to caller buffers (device pointers, canonical layout):

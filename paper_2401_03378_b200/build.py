@@ -14,6 +14,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libspark.so")
+# parity build: no FMA contraction, IEEE division / sqrt (R15/R16)
+STRICT_LIB = os.path.join(LIBDIR, "libspark_strict.so")
+STRICT_FLAGS = ("--fmad=false", "-DSPARK_STRICT_MATH")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -45,7 +48,21 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False, out: str = LIB, defs=()) -> str:
+def stale_lib(path: str) -> bool:
+    if not os.path.exists(path):
+        return True
+    t = os.path.getmtime(path)
+    return any(os.path.getmtime(f) > t for f in sources() + headers() + [__file__])
+
+
+def build_strict(force: bool = False) -> str:
+    """libspark_strict.so: the same sources with --fmad=false -DSPARK_STRICT_MATH."""
+    if not force and not stale_lib(STRICT_LIB):
+        return STRICT_LIB
+    return build(force=True, out=STRICT_LIB, flags=STRICT_FLAGS)
+
+
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defs=(), flags=()) -> str:
     """Build libspark.so (``out``/``defs``: design-experiment variants, tools/ablate.sh)."""
     if out == LIB and not force and not stale():
         return LIB
@@ -54,7 +71,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defs=()) -
     tmp = out + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
            "-Xptxas", "-v" if verbose else "-O3",
-           *[f"-D{d}" for d in defs], "-I", os.path.join(ROOT, "include"), "-I", inc, *sources(),
+           *flags, *[f"-D{d}" for d in defs], "-I", os.path.join(ROOT, "include"), "-I", inc, *sources(),
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-o", tmp]
     subprocess.check_call(cmd)
     os.replace(tmp, out)
@@ -64,4 +81,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defs=()) -
 if __name__ == "__main__":
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
     outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=outs[0] if outs else LIB, defs=defs))
+    if "--strict" in sys.argv:
+        print(build_strict(force="--force" in sys.argv))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=outs[0] if outs else LIB, defs=defs))

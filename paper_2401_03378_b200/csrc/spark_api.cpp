@@ -13,6 +13,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -355,9 +356,13 @@ void exchange_local(const std::vector<spark_ctx*>& m) {
     }
 }
 
+// One collective per step carries the CFL minimum AND the first failing step
+// (u64 pair, element-wise min), so the error decision is global: every rank
+// sees the same `bad` and rolls back (or reports) together.
+static_assert(offsetof(spark::DevScalars, bad) == offsetof(spark::DevScalars, acc) + 8, "acc/bad pair");
 void allreduce_acc(spark_ctx* c) {
     if (c->comm)
-        NC(ncclAllReduce(&c->sc->acc, &c->sc->acc, 1, ncclUint64, ncclMin, c->comm, c->stream));
+        NC(ncclAllReduce(&c->sc->acc, &c->sc->acc, 2, ncclUint64, ncclMin, c->comm, c->stream));
 }
 
 // Local group: every member's acc <- min over members (tiny host-side launch
@@ -432,22 +437,50 @@ int stage_buffers(int S, int n, int s, int* prev, int* out) {
     return S == 2 ? y : x;
 }
 
-void sync_and_check(spark_ctx* c, bool rollback_on_error, int old_n) {
+spark::DevScalars read_scalars(spark_ctx* c) {
     CU(cudaStreamSynchronize(c->stream));
     spark::DevScalars h;
     CU(cudaMemcpy(&h, c->sc, sizeof(h), cudaMemcpyDeviceToHost));
-    if (h.status & 1) {
-        if (rollback_on_error && old_n >= 0) {
-            c->n_idx = old_n;
-            h.t = h.t_prev;
-            h.steps -= 1;
-            h.acc = h.acc_prev;
-            h.status = 0;
-            CU(cudaMemcpy(c->sc, &h, sizeof(h), cudaMemcpyHostToDevice));
-            throw Error(SPARK_ERR_NONPHYSICAL, "non-physical state (rho<=0, p<=0 or NaN); rolled back to U^n");
-        }
-        throw Error(SPARK_ERR_NONPHYSICAL, "non-physical state (rho<=0, p<=0 or NaN)");
+    return h;
+}
+
+// Whether the step just executed (h read after it) is the one that failed on
+// some rank: only then can U^n of that step still be restored.
+bool failed_now(const spark::DevScalars& h) {
+    return h.bad != spark::kNoBad && h.active && h.bad == (unsigned long long)h.steps;
+}
+
+void rollback(spark_ctx* c, spark::DevScalars h, int old_n) {
+    c->n_idx = old_n;
+    h.t = h.t_prev;
+    h.steps -= 1;
+    h.acc = h.acc_prev;
+    h.bad = spark::kNoBad;
+    h.status = 0;
+    h.active = 1;
+    CU(cudaMemcpy(c->sc, &h, sizeof(h), cudaMemcpyHostToDevice));
+}
+
+[[noreturn]] void throw_nonphysical(const spark::DevScalars& h, bool rolled_back) {
+    const std::string where = (h.status & 1) ? " (seen on this rank)" : " (seen on another rank)";
+    if (rolled_back)
+        throw Error(SPARK_ERR_NONPHYSICAL, "non-physical state (rho<=0, p<=0 or NaN) in step " +
+                                               std::to_string(h.bad) + where + "; rolled back to U^n");
+    throw Error(SPARK_ERR_NONPHYSICAL, "non-physical state (rho<=0, p<=0 or NaN) in step " + std::to_string(h.bad) +
+                                           where + "; later steps were frozen, state not rolled back");
+}
+
+// Synchronise and check the GLOBAL failure word (reduced over ranks with the
+// CFL minimum).  old_n >= 0 and rollback_on_error: roll back when the step just
+// executed is the failing one; every rank decides identically.
+void sync_and_check(spark_ctx* c, bool rollback_on_error, int old_n) {
+    spark::DevScalars h = read_scalars(c);
+    if (h.bad == spark::kNoBad) return;
+    if (rollback_on_error && old_n >= 0 && failed_now(h)) {
+        rollback(c, h, old_n);
+        throw_nonphysical(h, true);
     }
+    throw_nonphysical(h, false);
 }
 
 void do_step(spark_ctx* c, double dt) {
@@ -701,6 +734,15 @@ spark_status spark_get_time(spark_ctx* ctx, double* t, int64_t* steps, double* d
     });
 }
 
+spark_status spark_set_time(spark_ctx* ctx, double t, int64_t steps) {
+    if (!ctx || !std::isfinite(t) || steps < 0) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        if (!ctx->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
+        set_device(ctx);
+        launched(ctx, spark::launch_set_time(ctx->sc, t, steps, ctx->stream), "set time");
+    });
+}
+
 spark_status spark_get_cfl_min(spark_ctx* ctx, double* value) {
     if (!ctx || !value) return SPARK_ERR_ARG;
     return guard(ctx, [&] {
@@ -819,10 +861,24 @@ spark_status spark_step_group(spark_ctx* const* ctxs, int32_t n, double dt, doub
             c->n_idx = stage_buffers(S, c->n_idx, 1, &pi, &po);
         }
         if (dt_used) {
-            for (int r = 0; r < n; r++) sync_and_check(m[r], true, old[r]);
-            double h;
-            CU(cudaMemcpy(&h, &c0->sc->dt, sizeof(double), cudaMemcpyDeviceToHost));
-            *dt_used = h;
+            // every member holds the group-min `bad`: decide once, then roll
+            // back all members or none before reporting
+            std::vector<spark::DevScalars> h(n);
+            for (int r = 0; r < n; r++) h[r] = read_scalars(m[r]);
+            if (h[0].bad != spark::kNoBad) {
+                const bool now = failed_now(h[0]);
+                for (int r = 0; r < n; r++)
+                    if (h[r].bad != h[0].bad || failed_now(h[r]) != now)
+                        throw Error(SPARK_ERR_STATE, "local group members disagree on the failure word");
+                if (now)
+                    for (int r = 0; r < n; r++) rollback(m[r], h[r], old[r]);
+                spark::DevScalars any = h[0];
+                for (int r = 0; r < n; r++) any.status |= h[r].status;
+                throw_nonphysical(any, now);
+            }
+            double h0;
+            CU(cudaMemcpy(&h0, &c0->sc->dt, sizeof(double), cudaMemcpyDeviceToHost));
+            *dt_used = h0;
         }
     });
 }

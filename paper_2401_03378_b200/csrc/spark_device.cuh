@@ -29,6 +29,24 @@ struct StencilOf {
 };
 
 // ------------------------------------------------------------ arithmetic
+#ifdef SPARK_STRICT_MATH
+// Parity build (libspark_strict.so, nvcc --fmad=false; DESIGN.md reading
+// R16/R15): no fused multiply-add anywhere (explicit fma() calls become a
+// rounded product plus a rounded sum, as the oracle's -ffp-contract=off C) and
+// IEEE division / square root instead of the MUFU + Newton forms below.
+__host__ __device__ __forceinline__ double spark_strict_fma(double a, double b, double c) {
+#ifdef __CUDA_ARCH__
+    return __dadd_rn(__dmul_rn(a, b), c);
+#else
+    volatile double p = a * b;
+    return p + c;
+#endif
+}
+#define fma(a, b, c) spark_strict_fma((a), (b), (c))
+__host__ __device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
+__host__ __device__ __forceinline__ double sqrt_fast(double a) { return sqrt(a); }
+__host__ __device__ __forceinline__ double rsqrt_fast(double a) { return 1.0 / sqrt(a); }
+#else
 // 1/x: MUFU seed (~2^-22) and one cubic Newton step y(1 + e + e^2), e = 1 - xy.
 __host__ __device__ __forceinline__ double rcp(double x) {
 #ifdef __CUDA_ARCH__
@@ -68,6 +86,7 @@ __host__ __device__ __forceinline__ double rsqrt_fast(double a) {
     const double r = fma(-a * y, y, 1.0);
     return fma(y * r, fma(0.375, r, 0.5), y);
 }
+#endif  // SPARK_STRICT_MATH
 
 // x > 0 for non-NaN x, on the integer pipe (+0 and -0 are not positive).
 __host__ __device__ __forceinline__ long long dbits(double x) {
@@ -459,6 +478,14 @@ __device__ __forceinline__ bool fetch_cons(const Geo& g, const double* __restric
     if (!fetch_src(g, u, halo, l0, l1, l2, s)) return false;
     load_src<NV>(s.p, s.vs, s.flip, out);
     return true;
+}
+
+// Record a non-physical state seen by this thread block in the step in
+// flight: the local status bit and the first failing step (global after the
+// per-step min-reduction of `bad`).
+__device__ __forceinline__ void flag_nonphysical(DevScalars* sc) {
+    atomicOr(&sc->status, 1);
+    atomicMin(&sc->bad, (unsigned long long)sc->steps);
 }
 
 // ------------------------------------------------------------ reductions

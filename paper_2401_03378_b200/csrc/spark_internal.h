@@ -10,14 +10,20 @@ namespace spark {
 constexpr int kMaxThreads = 1024;
 
 // Device-resident scalars of one context (one per rank).
+// The per-step collective reduces acc and bad together (two u64, ncclMin /
+// group min): every rank then sees the same CFL minimum AND the same first
+// failing step, so all ranks roll back (or report) together.
+constexpr unsigned long long kNoBad = ~0ull;
 struct DevScalars {
     double dt;                    // dt of the step in flight
     double t;                     // time at the end of the step in flight
     double t_prev;                // time at its start (rollback)
     unsigned long long acc;       // CFL min accumulator: bits of a positive double
+    unsigned long long bad;       // first step (value of `steps`) that produced a non-physical
+                                  // state on any rank (kNoBad: none); adjacent to acc
     unsigned long long acc_prev;  // value consumed by the step in flight (rollback)
-    int status;                   // bit 0: non-physical state seen
-    int active;                   // 0 once t >= t_end: stages copy U unchanged
+    int status;                   // bit 0: non-physical state seen on this rank
+    int active;                   // 0 once t >= t_end or after a failure: stages copy U unchanged
     long long steps;              // completed steps
     double pad[8];
 };
@@ -81,6 +87,7 @@ cudaError_t launch_pack(const Geo& g, const double* u, int dim, int side, double
 cudaError_t launch_fill_padded(const Geo& g, const double* u, const double* const halo[3][2], double* padded,
                                cudaStream_t s);
 cudaError_t launch_scalars_reset(DevScalars* sc, cudaStream_t s);
+cudaError_t launch_set_time(DevScalars* sc, double t, long long steps, cudaStream_t s);
 cudaError_t launch_group_min(const AccPtrs& p, int n, cudaStream_t s);
 cudaError_t launch_selftest_riemann(int riemann, int ndim, int dir, double gamma, int64_t n, const double* wl,
                                     const double* wr, double* f);

@@ -53,13 +53,15 @@ __global__ void cfl_min_kernel(const Geo g, const double* __restrict__ u, DevSca
         ok &= cons_to_prim<NV>(c, w, g.gamma - 1.0);
         m = fmin(m, cfl_term<NV>(g, w));
     }
-    if (!ok) atomicOr(&sc->status, 1);
+    if (!ok) flag_nonphysical(sc);
     block_min_to(m, red, &sc->acc);
 }
 
 __global__ void step_begin_kernel(DevScalars* sc, double dt_fixed, double t_end, double cfl) {
     const double t = sc->t;
-    if (dt_fixed <= 0.0 && t_end > 0.0 && t >= t_end * (1.0 - 1e-14)) {
+    // stop at t_end, and freeze after a non-physical state on any rank (the
+    // failure is reported, not rolled back, by the next synchronising call)
+    if ((dt_fixed <= 0.0 && t_end > 0.0 && t >= t_end * (1.0 - 1e-14)) || sc->bad != kNoBad) {
         sc->dt = 0.0;
         sc->active = 0;
         sc->t_prev = t;
@@ -82,10 +84,18 @@ __global__ void step_begin_kernel(DevScalars* sc, double dt_fixed, double t_end,
     sc->acc = 0x7ff0000000000000ull;  // +inf
 }
 
+// element-wise min of the (acc, bad) pairs of the members of a local group
 __global__ void group_min_kernel(const AccPtrs p, int n) {
+    const int e = threadIdx.x;  // 0: acc, 1: bad
     unsigned long long m = ~0ull;
-    for (int r = 0; r < n; r++) m = *p.p[r] < m ? *p.p[r] : m;
-    for (int r = 0; r < n; r++) *p.p[r] = m;
+    for (int r = 0; r < n; r++) m = p.p[r][e] < m ? p.p[r][e] : m;
+    for (int r = 0; r < n; r++) p.p[r][e] = m;
+}
+
+__global__ void set_time_kernel(DevScalars* sc, double t, long long steps) {
+    sc->t = t;
+    sc->t_prev = t;
+    sc->steps = steps;
 }
 
 __global__ void scalars_reset_kernel(DevScalars* sc) {
@@ -94,6 +104,7 @@ __global__ void scalars_reset_kernel(DevScalars* sc) {
     sc->t_prev = 0.0;
     sc->acc = 0x7ff0000000000000ull;
     sc->acc_prev = 0x7ff0000000000000ull;
+    sc->bad = kNoBad;
     sc->status = 0;
     sc->active = 1;
     sc->steps = 0;
@@ -215,7 +226,12 @@ cudaError_t launch_step_begin(DevScalars* sc, double dt_fixed, double t_end, dou
 }
 
 cudaError_t launch_group_min(const AccPtrs& p, int n, cudaStream_t s) {
-    group_min_kernel<<<1, 1, 0, s>>>(p, n);
+    group_min_kernel<<<1, 2, 0, s>>>(p, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_time(DevScalars* sc, double t, long long steps, cudaStream_t s) {
+    set_time_kernel<<<1, 1, 0, s>>>(sc, t, steps);
     return cudaGetLastError();
 }
 

@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
             }
         }
     }
-    if (!ok) atomicOr(&A.sc->status, 1);
+    if (!ok) flag_nonphysical(A.sc);
     if (A.last) {
         __syncthreads();
         block_min_to(cflmin, smem, &A.sc->acc);  // the planes are dead here

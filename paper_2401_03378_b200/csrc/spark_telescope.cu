@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kTeleThreads) telescope_kernel(const StageArgs
             }
         }
     }
-    if (!ok) atomicOr(&A.sc->status, 1);
+    if (!ok) flag_nonphysical(A.sc);
     __syncthreads();
     block_min_to(cflmin, red, &A.sc->acc);
 }

@@ -25,7 +25,7 @@ EXPORTS = [
     "spark_finalize", "spark_last_error", "spark_set_state", "spark_set_primitive", "spark_get_state",
     "spark_get_time", "spark_get_cfl_min", "spark_fill_guardcells", "spark_step", "spark_advance",
     "spark_step_group", "spark_stage_apply", "spark_profile_enable", "spark_profile_read",
-    "spark_selftest_riemann", "spark_axpy", "spark_step_telescoping", "spark_run",
+    "spark_selftest_riemann", "spark_axpy", "spark_step_telescoping", "spark_run", "spark_set_time",
 ]
 
 
@@ -115,6 +115,7 @@ def lib() -> ctypes.CDLL:
         "spark_get_state": (i32, [vp, vp, i32]),
         "spark_get_time": (i32, [vp, P(d), P(i64), P(d)]),
         "spark_get_cfl_min": (i32, [vp, P(d)]),
+        "spark_set_time": (i32, [vp, d, i64]),
         "spark_fill_guardcells": (i32, [vp, vp]),
         "spark_step": (i32, [vp, d, d, P(d)]),
         "spark_advance": (i32, [vp, i64, d, i32, P(i64)]),
@@ -337,6 +338,10 @@ class Spark:
         n = ctypes.c_int64()
         _check(lib().spark_get_time(self.ctx, ctypes.byref(t), ctypes.byref(n), ctypes.byref(dt)), self.ctx, "time")
         return t.value, n.value, dt.value
+
+    def set_time(self, t: float, steps: int):
+        """Restore t and the step count after set_state (checkpoint/resume)."""
+        _check(lib().spark_set_time(self.ctx, float(t), int(steps)), self.ctx, "set_time")
 
     def cfl_min(self) -> float:
         v = ctypes.c_double()

@@ -32,7 +32,7 @@ def test_library_exports_every_symbol():
     L = spark.lib()
     for name in header_functions():
         assert hasattr(L, name), name
-    assert L.spark_abi_version() == 2
+    assert L.spark_abi_version() == 3
 
 
 def test_sm100a_code_in_library():

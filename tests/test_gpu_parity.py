@@ -308,12 +308,15 @@ def test_nonphysical_rollback(sp):
     U2 = U.copy()
     U2[3, 2, 0, 5, 5] = -50.0  # negative total energy -> p < 0
     s.set_state(U2)
-    with pytest.raises(sp.NonPhysicalError):
+    # the LOADED state is non-physical (flagged as step 0 by set_state's CFL
+    # pass): steps are frozen and reported, nothing can be rolled back
+    with pytest.raises(sp.NonPhysicalError, match="step 0.*not rolled back"):
         s.step(dt=1e-4, sync=True)
-    # rolled back: U^n of the failed step is the current state, time unchanged
-    assert np.array_equal(state(s), U2)
     t, n, _ = s.time()
     assert t == 0.0 and n == 0
+    with pytest.raises(sp.NonPhysicalError):
+        state(s)
+    # (a step that itself fails is rolled back: tests/test_gpu_errors.py)
     # a physical state steps normally afterwards
     s.set_state(U)
     s.step(dt=1e-4, sync=True)
