@@ -60,6 +60,7 @@ class _Cfg(ctypes.Structure):
         ("gamma", ctypes.c_double),
         ("cfl", ctypes.c_double),
         ("grav", ctypes.c_double * 3),
+        ("shock_thresh", ctypes.c_double),
     ]
 
 
@@ -86,6 +87,7 @@ def lib():
             "oracle_weno5z_edge": (d, [d, d, d, d, d]),
             "oracle_weno5z_face": (None, [dp, dp, dp]),
             "oracle_riemann": (None, [i32, i32, d, dp, dp, dp]),
+            "oracle_shock_face": (i32, [dp, dp, d]),
             "oracle_dt_raw": (d, [P(_Cfg), dp]),
             "oracle_dt": (d, [P(_Cfg), dp, d, d]),
             "oracle_stage_padded": (i32, [P(_Cfg), dp, dp, d, d, d, dp]),
@@ -120,6 +122,7 @@ class Config:
     gamma: float = 1.4
     cfl: float = 0.8
     grav: tuple = (0.0, 0.0, 0.0)
+    shock_thresh: float = 0.0
     extra: dict = field(default_factory=dict)
 
     def c(self) -> _Cfg:
@@ -137,6 +140,7 @@ class Config:
         s.gamma, s.cfl = self.gamma, self.cfl
         for d in range(3):
             s.grav[d] = self.grav[d]
+        s.shock_thresh = self.shock_thresh
         return s
 
     @property
@@ -242,6 +246,14 @@ def weno5_face(s):
     l, r = ctypes.c_double(), ctypes.c_double()
     lib().oracle_weno5_face(_dp(s), ctypes.byref(l), ctypes.byref(r))
     return l.value, r.value
+
+
+def shock_face(un, p, thresh: float) -> bool:
+    """shockDet face flag from the normal velocity and pressure of the cells
+    i-1, i, i+1, i+2 of the face between cells i and i+1."""
+    un = np.ascontiguousarray(un, dtype=np.float64)
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    return bool(lib().oracle_shock_face(_dp(un), _dp(p), thresh))
 
 
 def riemann(kind: int, gamma: float, wl, wr) -> np.ndarray:

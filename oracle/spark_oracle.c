@@ -51,11 +51,12 @@ typedef struct {
     int32_t rk_stages;      /* 2 or 3 */
     double gamma, cfl;
     double grav[3];         /* grvAccel: uniform gravitational acceleration (0: none) */
+    double shock_thresh;    /* shockDet threshold (riemann 2 = HLLC, HLL at shock faces) */
 } ocfg;
 
 enum { OBC_PERIODIC = 0, OBC_OUTFLOW = 1, OBC_REFLECT = 2 };
 enum { OREC_FIRST = 0, OREC_PLM = 1, OREC_WENO5 = 2, OREC_PLM_MC = 3, OREC_WENO5Z = 4 };
-enum { ORS_HLL = 0, ORS_HLLC = 1 };
+enum { ORS_HLL = 0, ORS_HLLC = 1, ORS_HYBRID = 2 };
 
 /* status codes */
 enum { OK = 0, OERR_ARG = 1, OERR_NONPHYSICAL = 5, OERR_OOM = 4 };
@@ -88,7 +89,9 @@ int oracle_check_config(const ocfg* c) {
         if (d < c->ndim && c->nb[d] < c->ng) return OERR_ARG;
     }
     if (c->recon < 0 || c->recon > 4 || c->ng < ngk_of(c->recon)) return OERR_ARG;
-    if (c->riemann < 0 || c->riemann > 1) return OERR_ARG;
+    if (c->riemann < 0 || c->riemann > 2) return OERR_ARG;
+    /* shockDet reads the cells i-1..i+2 of a face: a stencil of 2 each side */
+    if (c->riemann == ORS_HYBRID && (ngk_of(c->recon) < 2 || !(c->shock_thresh > 0.0))) return OERR_ARG;
     if (c->rk_stages != 2 && c->rk_stages != 3) return OERR_ARG;
     if (!(c->gamma > 1.0) || !(c->cfl > 0.0)) return OERR_ARG;
     return OK;
@@ -317,6 +320,38 @@ static double grav_source(const ocfg* c, int v, const double* u) {
 
 static int has_grav(const ocfg* c) { return c->grav[0] != 0.0 || c->grav[1] != 0.0 || c->grav[2] != 0.0; }
 
+/* ----------------------------------------------------------------- shockDet */
+/* shockDet (Alg. 7; reading R21).  Cell i is a shock cell
+ * along direction d when the flow converges across it, u_d(i+1) < u_d(i-1),
+ * and the pressure jump across it is large, |p(i+1) - p(i-1)| > thresh *
+ * min(p(i-1), p(i+1)).  A face is a shock face when either of its two cells is
+ * a shock cell along the face normal.  Consumer (calcFlux, reading R21): the
+ * hybrid solver takes HLL at shock faces and HLLC elsewhere. */
+static int shock_cell(double um, double up, double pm, double pp, double thresh) {
+    if (!(up - um < 0.0)) return 0;
+    double pmin = pm < pp ? pm : pp;
+    return fabs(pp - pm) > thresh * pmin;
+}
+
+/* un[m], p[m]: normal velocity and pressure of the cells i-1, i, i+1, i+2 of
+ * the face between cells i and i+1. */
+int oracle_shock_face(const double* un, const double* p, double thresh) {
+    return shock_cell(un[0], un[2], p[0], p[2], thresh) || shock_cell(un[1], un[3], p[1], p[3], thresh);
+}
+
+/* Riemann solver of a face whose stencil st (rotated frame, cells
+ * i-ngk+1..i+ngk, nv components each) is given: the configured one, or for
+ * the hybrid solver HLL at shock faces and HLLC elsewhere. */
+static int face_solver(const ocfg* c, int ngk, int nv, const double* st) {
+    if (c->riemann != ORS_HYBRID) return c->riemann;
+    double un[4], p[4];
+    for (int m = 0; m < 4; m++) {
+        un[m] = st[(ngk - 2 + m) * nv + 1];
+        p[m] = st[(ngk - 2 + m) * nv + nv - 1];
+    }
+    return oracle_shock_face(un, p, c->shock_thresh) ? ORS_HLL : ORS_HLLC;
+}
+
 /* ------------------------------------------------------------------ Riemann */
 /* Physical flux along the normal of the rotated frame (rho, u_n, u_t.., p).
  * ax[e] is the rotated index of axis e: |u|^2 is summed in axis order
@@ -479,7 +514,7 @@ int oracle_stage_padded(const ocfg* c, const double* P, const double* Un, double
                                 for (int v = 0; v < nv; v++) st[m * nv + v] = W[(long)rot[v] * np + q];
                             }
                             reconstruct(c->recon, ngk, nv, st, wl, wr);
-                            riemann_ax(c->riemann, nv, c->gamma, ax, wl, wr, fr);
+                            riemann_ax(face_solver(c, ngk, nv, st), nv, c->gamma, ax, wl, wr, fr);
                             long fidx = ((long)k * fn[1] + j) * fn[0] + i;
                             for (int v = 0; v < nv; v++) F[d][(long)rot[v] * nf[d] + fidx] = fr[v];
                         }
@@ -718,7 +753,7 @@ int oracle_step_telescoping(const ocfg* c, double* U, double t, double t_end, do
                                     for (int v = 0; v < nv; v++) st[m * nv + v] = W[(long)rot[v] * np + q];
                                 }
                                 reconstruct(c->recon, ngk, nv, st, wl, wr);
-                                riemann_ax(c->riemann, nv, c->gamma, ax, wl, wr, fr);
+                                riemann_ax(face_solver(c, ngk, nv, st), nv, c->gamma, ax, wl, wr, fr);
                                 for (int v = 0; v < nv; v++) F[d][(long)rot[v] * np + right] = fr[v];
                             }
                 }

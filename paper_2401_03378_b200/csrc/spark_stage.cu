@@ -108,7 +108,11 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
 #ifdef EXP_NOFUSE
     constexpr bool FUSE = false;
 #else
+#ifdef EXP_FCFUSE
+    constexpr bool FUSE = NBX == 16 && NBY == 16 && NDIM == 3;
+#else
     constexpr bool FUSE = NBX == 16 && NBY == 16 && NDIM == 3 && !FC;
+#endif
 #endif
     constexpr int NV = NDIM + 2;
     constexpr int NG = StencilOf<RECON>::NG;

@@ -54,6 +54,7 @@ class CConfig(ctypes.Structure):
         ("gamma", ctypes.c_double),
         ("cfl", ctypes.c_double),
         ("grav", ctypes.c_double * 3),
+        ("shock_thresh", ctypes.c_double),
     ]
 
 
@@ -81,6 +82,7 @@ def to_cconfig(cfg: dict) -> CConfig:
     c.cfl = float(cfg.get("cfl", 0.8))
     for d in range(3):
         c.grav[d] = float(cfg.get("grav", (0.0,) * 3)[d])
+    c.shock_thresh = float(cfg.get("shock_thresh", 0.0))
     return c
 
 

@@ -27,7 +27,7 @@ import numpy as np
 
 BC_PERIODIC, BC_OUTFLOW, BC_REFLECT = 0, 1, 2
 RECON_FIRST, RECON_PLM, RECON_WENO5, RECON_PLM_MC, RECON_WENO5Z = 0, 1, 2, 3, 4
-RIEMANN_HLL, RIEMANN_HLLC = 0, 1
+RIEMANN_HLL, RIEMANN_HLLC, RIEMANN_HYBRID = 0, 1, 2
 
 
 @dataclass(frozen=True)
@@ -50,12 +50,13 @@ class Problem:
     ic: str = "sod"
     t_end: float = 0.0
     grav: tuple = (0.0, 0.0, 0.0)
+    shock_thresh: float = 0.0
 
     def config(self) -> dict:
         return dict(ndim=self.ndim, nb=tuple(self.nb), nblk=tuple(self.nblk), ng=self.ng, lo=tuple(self.lo),
                     hi=tuple(self.hi), bc=tuple(tuple(x) for x in self.bc), recon=self.recon,
                     riemann=self.riemann, rk_stages=self.rk_stages, gamma=self.gamma, cfl=self.cfl,
-                    grav=tuple(self.grav))
+                    grav=tuple(self.grav), shock_thresh=self.shock_thresh)
 
     def with_(self, **kw) -> "Problem":
         return replace(self, **kw)
