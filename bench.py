@@ -162,6 +162,11 @@ def problem_for(args, world: int) -> si.Problem:
             p = p.with_(name=f"{p.name}+{args.recon}", recon=r, ng=max(p.ng, 3 if r in (2, 4) else (2 if r in (1, 3) else 1)))
     if getattr(args, "grav", None):
         p = p.with_(grav=tuple(float(x) for x in args.grav.split(",")))
+    if getattr(args, "riemann", None):
+        r = {"hll": si.RIEMANN_HLL, "hllc": si.RIEMANN_HLLC, "hybrid": si.RIEMANN_HYBRID}[args.riemann]
+        if r != p.riemann:
+            p = p.with_(name=f"{p.name}+{args.riemann}", riemann=r,
+                        shock_thresh=args.shock_thresh if r == si.RIEMANN_HYBRID else 0.0)
     if world > 1 and args.scaling == "weak":
         # weak scaling: 256^3 (16^3 blocks of 16^3) per GPU along a process grid
         pg = {2: (1, 1, 2), 4: (1, 2, 2), 8: (2, 2, 2)}.get(world)
@@ -240,6 +245,9 @@ def main():
     ap.add_argument("--recon", default=None, choices=["first", "plm", "weno5", "mc", "wenoz"],
                     help="override the config's reconstruction (NEXT N2: mc = PLM-MC, wenoz = WENO5-Z)")
     ap.add_argument("--grav", default=None, help="uniform gravity gx,gy,gz (grvAccel, NEXT N2)")
+    ap.add_argument("--riemann", default=None, choices=["hll", "hllc", "hybrid"],
+                    help="override the Riemann solver (hybrid = shockDet + HLL at shock faces, NEXT N2)")
+    ap.add_argument("--shock-thresh", type=float, default=0.5, help="shockDet threshold for --riemann hybrid")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = the config's grid per GPU; strong = the config's grid split over N")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -468,7 +476,7 @@ def main():
             "config": {"workload": p.name, "cells": p.ncells, "cells_per_gpu": cells_local,
                        "block": list(p.nb), "blocks": list(p.nblk),
                        "recon": ["first", "plm", "weno5", "plm_mc", "weno5z"][p.recon], "grav": list(p.grav),
-                       "riemann": ["hll", "hllc"][p.riemann], "rk_stages": p.rk_stages, "ng": p.ng,
+                       "riemann": ["hll", "hllc", "hybrid"][p.riemann], "rk_stages": p.rk_stages, "ng": p.ng,
                        "parallelism": f"blocks over {world} GPU(s)", "l2": "state per copy > L2 (no flush needed)",
                        "rk_mode": "telescoping" if args.telescoping else "non-telescoping",
                        "launch": "cuda-graph (spark_run)" if args.graphs else "stream (spark_step)"},

@@ -70,7 +70,9 @@ typedef enum {
     SPARK_RECON_PLM_MC = 3,
     SPARK_RECON_WENO5Z = 4
 } spark_recon;
-typedef enum { SPARK_RIEMANN_HLL = 0, SPARK_RIEMANN_HLLC = 1 } spark_riemann;
+/* HYBRID (shockDet Alg. 7; reading R21): HLLC, but HLL at
+ * faces the shock detector flags (needs recon PLM, PLM_MC, WENO5 or WENO5Z). */
+typedef enum { SPARK_RIEMANN_HLL = 0, SPARK_RIEMANN_HLLC = 1, SPARK_RIEMANN_HYBRID = 2 } spark_riemann;
 
 /* Problem description.  Identical on every rank (it describes the GLOBAL grid). */
 typedef struct {
@@ -87,6 +89,10 @@ typedef struct {
     double cfl;           /* Courant number C in dt = C min dx_d/(|u_d| + c)         */
     double grav[3];       /* grvAccel (Alg. 8; reading R20): uniform gravity;
                            * L(U) += (0, rho g, m.g); all zero = no source. ABI v2  */
+    double shock_thresh;  /* shockDet (reading R21), used with SPARK_RIEMANN_HYBRID:
+                           * cell i is a shock cell along d when u_d(i+1) < u_d(i-1)
+                           * and |p(i+1) - p(i-1)| > shock_thresh * min(p(i+-1));
+                           * a face of a shock cell takes HLL.  > 0.  ABI v3          */
 } spark_config;
 
 typedef struct spark_ctx spark_ctx; /* opaque, one per rank (per GPU) */

@@ -87,7 +87,7 @@ def lib():
             "oracle_weno5z_edge": (d, [d, d, d, d, d]),
             "oracle_weno5z_face": (None, [dp, dp, dp]),
             "oracle_riemann": (None, [i32, i32, d, dp, dp, dp]),
-            "oracle_shock_face": (i32, [dp, dp, d]),
+            "oracle_shock_face": (i32, [dp, dp, dp, d, d]),
             "oracle_dt_raw": (d, [P(_Cfg), dp]),
             "oracle_dt": (d, [P(_Cfg), dp, d, d]),
             "oracle_stage_padded": (i32, [P(_Cfg), dp, dp, d, d, d, dp]),
@@ -248,12 +248,13 @@ def weno5_face(s):
     return l.value, r.value
 
 
-def shock_face(un, p, thresh: float) -> bool:
-    """shockDet face flag from the normal velocity and pressure of the cells
-    i-1, i, i+1, i+2 of the face between cells i and i+1."""
+def shock_face(un, p, thresh: float, rho=(1.0, 1.0, 1.0, 1.0), gamma: float = 1.4) -> bool:
+    """shockDet face flag from the normal velocity, pressure and density of the
+    cells i-1, i, i+1, i+2 of the face between cells i and i+1."""
     un = np.ascontiguousarray(un, dtype=np.float64)
     p = np.ascontiguousarray(p, dtype=np.float64)
-    return bool(lib().oracle_shock_face(_dp(un), _dp(p), thresh))
+    rho = np.ascontiguousarray(rho, dtype=np.float64)
+    return bool(lib().oracle_shock_face(_dp(un), _dp(p), _dp(rho), thresh, gamma))
 
 
 def riemann(kind: int, gamma: float, wl, wr) -> np.ndarray:

@@ -322,21 +322,34 @@ static int has_grav(const ocfg* c) { return c->grav[0] != 0.0 || c->grav[1] != 0
 
 /* ----------------------------------------------------------------- shockDet */
 /* shockDet (Alg. 7; reading R21).  Cell i is a shock cell
- * along direction d when the flow converges across it, u_d(i+1) < u_d(i-1),
- * and the pressure jump across it is large, |p(i+1) - p(i-1)| > thresh *
- * min(p(i-1), p(i+1)).  A face is a shock face when either of its two cells is
- * a shock cell along the face normal.  Consumer (calcFlux, reading R21): the
- * hybrid solver takes HLL at shock faces and HLLC elsewhere. */
-static int shock_cell(double um, double up, double pm, double pp, double thresh) {
-    if (!(up - um < 0.0)) return 0;
+ * along direction d when
+ *   (a) the flow converges across it faster than a dead band of 1e-6 of the
+ *       sound speed: u_d(i+1) - u_d(i-1) < -1e-6 c, with
+ *       c^2 = gamma max(p(i-1)/rho(i-1), p(i+1)/rho(i+1)) — symmetric states
+ *       leave velocities that are exactly equal or exactly zero, and their
+ *       last-bit noise must not decide a shock; a real shock compresses by O(c);
+ *   (b) the pressure jump across it is large:
+ *       |p(i+1) - p(i-1)| > thresh * min(p(i-1), p(i+1)).
+ * (a) is evaluated without division as d < 0 and
+ * d^2 rho(i-1) rho(i+1) > 1e-12 gamma max(p(i-1) rho(i+1), p(i+1) rho(i-1)).
+ * A face is a shock face when either of its two cells is a shock cell along
+ * the face normal.  Consumer (calcFlux, reading R21): the hybrid solver takes
+ * HLL at shock faces and HLLC elsewhere. */
+static int shock_cell(double um, double up, double pm, double pp, double rm, double rp, double thresh,
+                      double gamma) {
+    double d = up - um;
+    if (!(d < 0.0)) return 0;
+    double a = pm * rp, b = pp * rm;
+    if (!(d * d * (rm * rp) > 1e-12 * gamma * (a > b ? a : b))) return 0;
     double pmin = pm < pp ? pm : pp;
     return fabs(pp - pm) > thresh * pmin;
 }
 
-/* un[m], p[m]: normal velocity and pressure of the cells i-1, i, i+1, i+2 of
- * the face between cells i and i+1. */
-int oracle_shock_face(const double* un, const double* p, double thresh) {
-    return shock_cell(un[0], un[2], p[0], p[2], thresh) || shock_cell(un[1], un[3], p[1], p[3], thresh);
+/* un[m], p[m], rho[m]: normal velocity, pressure and density of the cells
+ * i-1, i, i+1, i+2 of the face between cells i and i+1. */
+int oracle_shock_face(const double* un, const double* p, const double* rho, double thresh, double gamma) {
+    return shock_cell(un[0], un[2], p[0], p[2], rho[0], rho[2], thresh, gamma) ||
+           shock_cell(un[1], un[3], p[1], p[3], rho[1], rho[3], thresh, gamma);
 }
 
 /* Riemann solver of a face whose stencil st (rotated frame, cells
@@ -344,12 +357,13 @@ int oracle_shock_face(const double* un, const double* p, double thresh) {
  * the hybrid solver HLL at shock faces and HLLC elsewhere. */
 static int face_solver(const ocfg* c, int ngk, int nv, const double* st) {
     if (c->riemann != ORS_HYBRID) return c->riemann;
-    double un[4], p[4];
+    double un[4], p[4], rho[4];
     for (int m = 0; m < 4; m++) {
+        rho[m] = st[(ngk - 2 + m) * nv + 0];
         un[m] = st[(ngk - 2 + m) * nv + 1];
         p[m] = st[(ngk - 2 + m) * nv + nv - 1];
     }
-    return oracle_shock_face(un, p, c->shock_thresh) ? ORS_HLL : ORS_HLLC;
+    return oracle_shock_face(un, p, rho, c->shock_thresh, c->gamma) ? ORS_HLL : ORS_HLLC;
 }
 
 /* ------------------------------------------------------------------ Riemann */

@@ -59,7 +59,12 @@ std::string check(const spark_config* c, int nranks) {
     for (int d = 0; d < 3; d++)
         if (!std::isfinite(c->grav[d]) || (d >= c->ndim && c->grav[d] != 0.0))
             return "grav must be finite and zero along unused dims";
-    if (c->riemann < 0 || c->riemann > 1) return "unknown riemann";
+    if (c->riemann < 0 || c->riemann > 2) return "unknown riemann";
+    if (c->riemann == SPARK_RIEMANN_HYBRID) {
+        // shockDet reads the cells i-1..i+2 of a face (reading R21)
+        if (stencil_ng(c->recon) < 2) return "the hybrid Riemann solver (shockDet) needs recon PLM, PLM-MC or WENO5";
+        if (!(c->shock_thresh > 0.0) || !std::isfinite(c->shock_thresh)) return "shock_thresh must be finite and > 0";
+    }
     if (c->rk_stages != 2 && c->rk_stages != 3) return "rk_stages must be 2 or 3";
     if (!(c->gamma > 1.0)) return "gamma must be > 1";
     if (!(c->cfl > 0.0)) return "cfl must be > 0";
@@ -189,6 +194,7 @@ Plan make_plan(const spark_config* c, int rank, int nranks, bool self_exchange =
     if (g.ncell >= (1LL << 31)) throw Error(SPARK_ERR_ARG, "sub-box exceeds 2^31 cells (split over more ranks)");
     g.gamma = c->gamma;
     g.cfl = c->cfl;
+    g.shock_thresh = c->riemann == SPARK_RIEMANN_HYBRID ? c->shock_thresh : 0.0;
     g.has_grav = 0;
     for (int d = 0; d < 3; d++) {
         g.grav[d] = c->grav[d];

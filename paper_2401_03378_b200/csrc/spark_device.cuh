@@ -369,6 +369,53 @@ __host__ __device__ __forceinline__ void riemann(const double* wl, const double*
     }
 }
 
+// ------------------------------------------------------------- shockDet
+// shockDet (Alg. 7; reading R21): cell i is a shock cell along the
+// face normal when the flow converges across it by more than 1e-6 of the sound
+// speed, d = u(i+1) - u(i-1) < 0 with d^2 rho(i-1) rho(i+1) > 1e-12 gamma
+// max(p(i-1) rho(i+1), p(i+1) rho(i-1)) (no division; the dead band keeps the
+// exact ties and last-bit noise of symmetric states unflagged), and the
+// pressure jump across it exceeds thr * min(p(i-1), p(i+1)).  Evaluated on the
+// cell-centre primitives the face's reconstruction already reads.  Products
+// are rounded separately (never contracted), as in the oracle.
+__host__ __device__ __forceinline__ double dmul(double a, double b) {
+#ifdef __CUDA_ARCH__
+    return __dmul_rn(a, b);
+#else
+    return a * b;
+#endif
+}
+__host__ __device__ __forceinline__ bool shock_cell(double um, double up, double pm, double pp, double rm, double rp,
+                                                    double thr, double gamma) {
+    const double d = up - um;
+    const double a = dmul(pm, rp), b = dmul(pp, rm);
+    const double pmin = pm < pp ? pm : pp;
+    return (d < 0.0) & (dmul(dmul(d, d), dmul(rm, rp)) > dmul(dmul(1e-12, gamma), a > b ? a : b)) &
+           (fabs(pp - pm) > dmul(thr, pmin));
+}
+// face between cells i and i+1 from (u, p, rho) of the cells i-1, i, i+1, i+2
+__host__ __device__ __forceinline__ bool shock_face(const double* u, const double* p, const double* r, double thr,
+                                                    double gamma) {
+#ifdef EXP_SHK_ALL
+    return true;
+#endif
+    return shock_cell(u[0], u[2], p[0], p[2], r[0], r[2], thr, gamma) |
+           shock_cell(u[1], u[3], p[1], p[3], r[1], r[3], thr, gamma);
+}
+
+// calcFlux of one face: RS 0 HLL, 1 HLLC, 2 hybrid (HLL at shock faces,
+// HLLC elsewhere; the flag is only read for RS 2)
+template <int NV, int RS, int D>
+__host__ __device__ __forceinline__ void face_flux(const double* wl, const double* wr, bool shock, double gamma,
+                                                   double gm1i, double* f) {
+    if constexpr (RS == 2) {
+        if (shock) riemann<NV, 0, D>(wl, wr, gamma, gm1i, f);
+        else riemann<NV, 1, D>(wl, wr, gamma, gm1i, f);
+    } else {
+        riemann<NV, RS, D>(wl, wr, gamma, gm1i, f);
+    }
+}
+
 // grvAccel source (reading R20) of variable v at a cell with conserved value u
 // of that variable, called in variable order: rho and m.g accumulate in
 // (rho, mg).  S = (0, rho g, m.g).

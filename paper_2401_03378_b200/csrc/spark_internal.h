@@ -52,6 +52,7 @@ struct Geo {
     double gamma, cfl;
     double grav[3];               // grvAccel source (reading R20)
     int has_grav;                 // any grav[d] != 0
+    double shock_thresh;          // shockDet threshold (riemann 2, reading R21)
 };
 
 struct StageArgs {

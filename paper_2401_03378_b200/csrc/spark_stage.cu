@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     const double dt = A.dt_ptr ? *A.dt_ptr : A.dt_value;
     const double a = A.a, bco = A.b;
     const double gamma = g.gamma, gm1 = g.gamma - 1.0, gm1i = 1.0 / (g.gamma - 1.0);
+    const double thr = g.shock_thresh;  // shockDet (RS 2 only)
 
     if (A.part) {  // interior / rank-boundary split (CTA-uniform early exit)
         const bool edge = (g.halo[0][0] && bx == 0) || (g.halo[0][1] && bx == g.bn[0] - 1) ||
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
         }
     };
     // flux through the z face between cells z and z+1 of this column
-    auto zflux = [&](int z, double* wl, double* wr, double* f) {
+    auto zflux = [&](int z, double* wl, double* wr, bool shk, double* f) {
         if (RECON != 0 && !(positive(wl[0]) && positive(wl[NV - 1]) && positive(wr[0]) && positive(wr[NV - 1]))) {
 #pragma unroll
             for (int v = 0; v < NV; v++) {
@@ -273,7 +274,37 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                 wr[v] = ring_at(z + 1, v);
             }
         }
-        riemann<NV, RS, 2>(wl, wr, gamma, gm1i, f);
+        face_flux<NV, RS, 2>(wl, wr, shk, gamma, gm1i, f);
+    };
+    // shockDet along z (RS 2): shock cell z of this column from the ring
+    // (planes z-1, z+1); a z face's flag is the OR of its two cells, the lower
+    // one carried from the previous plane (the ring no longer holds plane z-1
+    // when face z+1/2 is solved)
+    auto zshock_cell = [&](int z) -> bool {
+        if constexpr (RS != 2) return false;
+#ifdef EXP_SHK_ALL
+        else return true;
+#else
+        else return shock_cell(ring_at(z - 1, NV - 2), ring_at(z + 1, NV - 2), ring_at(z - 1, NV - 1),
+                               ring_at(z + 1, NV - 1), ring_at(z - 1, 0), ring_at(z + 1, 0), thr, gamma);
+#endif
+    };
+    bool zs_prev = false;  // shock cell flag of the current plane (z)
+    // shockDet at an x or y face (RS 2): c = cell i+1 of the face (variable 0
+    // of the working plane), st the stride along the normal, vn the normal
+    // velocity's variable
+    auto shk_at = [&](const double* c, int st, int vn) -> bool {
+        if constexpr (RS != 2) return false;
+        else {
+            double u[4], pr[4], r[4];
+#pragma unroll
+            for (int m = 0; m < 4; m++) {
+                u[m] = c[vn * CP + (m - 2) * st];
+                pr[m] = c[(NV - 1) * CP + (m - 2) * st];
+                r[m] = c[(m - 2) * st];
+            }
+            return shock_face(u, pr, r, thr, gamma);
+        }
     };
 
     if (NDIM == 3) {
@@ -286,11 +317,13 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
             }
             double lo[NV], hi[NV], l0[NV];
             zrecon(-1, l0, hi);  // top edge of cell -1 -> L state of face -1/2
+            const bool zs_m1 = zshock_cell(-1);  // planes -2, 0 (before plane -NG dies)
             load_prim(ti, tj, NG - 1, w);  // replaces plane -NG (dead)
 #pragma unroll
             for (int v = 0; v < NV; v++) ring_at(NG - 1, v) = w[v];
             zrecon(0, lo, zhi);  // bottom edge of cell 0 -> R state of face -1/2
-            zflux(-1, hi, lo, fzlo);
+            zs_prev = zshock_cell(0);
+            zflux(-1, hi, lo, zs_m1 || zs_prev, fzlo);
         }
     }
 
@@ -564,6 +597,12 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
         // ---------------------------------------------------------------- S3
         // x face at column f of row r: cells (f-1, f); y face at row f of column r
         double fxo[NV], fyo[NV];  // this thread's own x / y face fluxes (OWNF)
+        bool zsh = false;         // shockDet flag of the z face kk+1/2 (RS 2)
+        if (NDIM == 3 && RS == 2 && live) {
+            const bool zs_next = zshock_cell(kk + 1);
+            zsh = zs_prev || zs_next;
+            zs_prev = zs_next;
+        }
         auto xface = [&](int r, int f, double* fl) {
             double wl[NV], wr[NV];
 #pragma unroll
@@ -583,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     wr[v] = cur[v * CP + (r + RO) * cw + f + NG];
                 }
             }
-            riemann<NV, RS, 0>(wl, wr, gamma, gm1i, fl);
+            face_flux<NV, RS, 0>(wl, wr, shk_at(cur + (r + RO) * cw + f + NG, 1, 1), gamma, gm1i, fl);
 #pragma unroll
             for (int v = 0; v < NV; v++) XA[v * fxn + r * fxs + f] = fl[v];
         };
@@ -606,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     wr[v] = cur[v * CP + (f + NG) * cw + r + NG];
                 }
             }
-            riemann<NV, RS, 1>(wl, wr, gamma, gm1i, fl);
+            face_flux<NV, RS, 1>(wl, wr, shk_at(cur + (f + NG) * cw + r + NG, cw, 2), gamma, gm1i, fl);
 #pragma unroll
             for (int v = 0; v < NV; v++) YA[v * fyn + f * nb0 + r] = fl[v];
         };
@@ -649,8 +688,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     }
                 }
             }
-            riemann<NV, RS, 0>(xl, xr, gamma, gm1i, fx);
-            riemann<NV, RS, 1>(yl, yr, gamma, gm1i, fy);
+            face_flux<NV, RS, 0>(xl, xr, shk_at(cur + (tj + RO) * cw + ti + 1 + NG, 1, 1), gamma, gm1i, fx);
+            face_flux<NV, RS, 1>(yl, yr, shk_at(cur + (tj + 1 + NG) * cw + ti + NG, cw, 2), gamma, gm1i, fy);
 #pragma unroll
             for (int v = 0; v < NV; v++) {
                 XA[v * fxn + xo] = fx[v];
@@ -675,6 +714,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                 const bool isy = tid >= 16;
                 const int q = tid & 15;
                 double bl[NV], br[NV], fb[NV];
+                const bool bshk = shk_at(isy ? cur + NG * cw + q + NG : cur + (q + RO) * cw + NG, isy ? cw : 1,
+                                         isy ? 2 : 1);
 #pragma unroll
                 for (int v = 0; v < NV; v++) {
                     if (FC) {  // face 0 of row / column q from cells -2..1
@@ -700,8 +741,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     br[1] = isy ? br[2] : r1;
                     br[2] = isy ? r1 : br[2];
                 }
-                if (NDIM == 3) riemann<NV, RS, 2>(zhi, zlo, gamma, gm1i, fzhi);
-                riemann<NV, RS, 0>(bl, br, gamma, gm1i, fb);
+                if (NDIM == 3) face_flux<NV, RS, 2>(zhi, zlo, zsh, gamma, gm1i, fzhi);
+                face_flux<NV, RS, 0>(bl, br, bshk, gamma, gm1i, fb);
                 {
                     const double f1 = fb[1];
                     fb[1] = isy ? fb[2] : f1;
@@ -713,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     else XA[v * fxn + q * fxs] = fb[v];
                 }
             } else if (NDIM == 3) {
-                riemann<NV, RS, 2>(zhi, zlo, gamma, gm1i, fzhi);
+                face_flux<NV, RS, 2>(zhi, zlo, zsh, gamma, gm1i, fzhi);
             }
             if (NDIM == 3) {
 #pragma unroll
@@ -725,7 +766,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     xface(tj, ti + 1, fxo);
                     if (NDIM >= 2) yface(ti, tj + 1, fyo);
                     if (NDIM == 3) {
-                        zflux(kk, zhi, zlo, fzhi);
+                        zflux(kk, zhi, zlo, zsh, fzhi);
 #pragma unroll
                         for (int v = 0; v < NV; v++) zhi[v] = zhn[v];
                     }
@@ -743,6 +784,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                         const bool isy = tid >= 16;
                         const int q = tid & 15;
                         double bl[NV], br[NV], fb[NV];
+                        const bool bshk = shk_at(isy ? cur + NG * cw + q + NG : cur + (q + RO) * cw + NG,
+                                                 isy ? cw : 1, isy ? 2 : 1);
 #pragma unroll
                         for (int v = 0; v < NV; v++) {
                             const double* c = cur + v * CP + (isy ? NG * cw + q + NG : (q + RO) * cw + NG);
@@ -763,7 +806,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                             br[1] = isy ? br[2] : r1;
                             br[2] = isy ? r1 : br[2];
                         }
-                        riemann<NV, RS, 0>(bl, br, gamma, gm1i, fb);
+                        face_flux<NV, RS, 0>(bl, br, bshk, gamma, gm1i, fb);
                         {
                             const double f1 = fb[1];
                             fb[1] = isy ? fb[2] : f1;
@@ -870,13 +913,20 @@ cudaError_t launch_shape(const StageArgs& a, cudaStream_t s) {
     return launch_t<NDIM, RECON, RS, 0, 0, 0>(a, s);
 }
 
+template <int NDIM, int RECON>
+cudaError_t launch_r(const StageArgs& a, int riemann, cudaStream_t s) {
+    if (riemann == 0) return launch_shape<NDIM, RECON, 0>(a, s);
+    if (riemann == 1 || RECON == 0) return launch_shape<NDIM, RECON, 1>(a, s);  // hybrid needs recon >= PLM
+    return launch_shape<NDIM, RECON, 2>(a, s);
+}
+
 template <int NDIM>
 cudaError_t launch_d(const StageArgs& a, int recon, int riemann, cudaStream_t s) {
-    if (recon == 0) return riemann ? launch_shape<NDIM, 0, 1>(a, s) : launch_shape<NDIM, 0, 0>(a, s);
-    if (recon == 1) return riemann ? launch_shape<NDIM, 1, 1>(a, s) : launch_shape<NDIM, 1, 0>(a, s);
-    if (recon == 3) return riemann ? launch_shape<NDIM, 3, 1>(a, s) : launch_shape<NDIM, 3, 0>(a, s);
-    if (recon == 4) return riemann ? launch_shape<NDIM, 4, 1>(a, s) : launch_shape<NDIM, 4, 0>(a, s);
-    return riemann ? launch_shape<NDIM, 2, 1>(a, s) : launch_shape<NDIM, 2, 0>(a, s);
+    if (recon == 0) return launch_r<NDIM, 0>(a, riemann, s);
+    if (recon == 1) return launch_r<NDIM, 1>(a, riemann, s);
+    if (recon == 3) return launch_r<NDIM, 3>(a, riemann, s);
+    if (recon == 4) return launch_r<NDIM, 4>(a, riemann, s);
+    return launch_r<NDIM, 2>(a, riemann, s);
 }
 
 }  // namespace

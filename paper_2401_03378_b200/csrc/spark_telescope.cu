@@ -129,12 +129,24 @@ __global__ void __launch_bounds__(kTeleThreads) telescope_kernel(const StageArgs
                     wr[v] = W[v * T + right];
                 }
             }
+            bool shk = false;  // shockDet (RS 2): cells right-2..right+1 along the normal
+            if constexpr (RS == 2) {
+                const int vn = xd ? 1 : 2, vp = NV - 1;
+                double u[4], pr[4], r[4];
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    u[m] = W[vn * T + right + (m - 2) * stride];
+                    pr[m] = W[vp * T + right + (m - 2) * stride];
+                    r[m] = W[right + (m - 2) * stride];
+                }
+                shk = shock_face(u, pr, r, A.g.shock_thresh, gamma);
+            }
             if (xd) {
-                riemann<NV, RS, 0>(wl, wr, gamma, gm1i, fl);
+                face_flux<NV, RS, 0>(wl, wr, shk, gamma, gm1i, fl);
 #pragma unroll
                 for (int v = 0; v < NV; v++) Fx[v * ty * (tx + 1) + j * (tx + 1) + i] = fl[v];
             } else {
-                riemann<NV, RS, (NDIM >= 2 ? 1 : 0)>(wl, wr, gamma, gm1i, fl);
+                face_flux<NV, RS, (NDIM >= 2 ? 1 : 0)>(wl, wr, shk, gamma, gm1i, fl);
 #pragma unroll
                 for (int v = 0; v < NV; v++) Fy[v * (ty + 1) * tx + j * tx + i] = fl[v];
             }
@@ -191,13 +203,20 @@ cudaError_t launch_t(const StageArgs& a, int S, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int NDIM, int RECON>
+cudaError_t launch_r(const StageArgs& a, int riemann, int S, cudaStream_t s) {
+    if (riemann == 0) return launch_t<NDIM, RECON, 0>(a, S, s);
+    if (riemann == 1 || RECON == 0) return launch_t<NDIM, RECON, 1>(a, S, s);  // hybrid needs recon >= PLM
+    return launch_t<NDIM, RECON, 2>(a, S, s);
+}
+
 template <int NDIM>
 cudaError_t launch_d(const StageArgs& a, int recon, int riemann, int S, cudaStream_t s) {
-    if (recon == 0) return riemann ? launch_t<NDIM, 0, 1>(a, S, s) : launch_t<NDIM, 0, 0>(a, S, s);
-    if (recon == 1) return riemann ? launch_t<NDIM, 1, 1>(a, S, s) : launch_t<NDIM, 1, 0>(a, S, s);
-    if (recon == 3) return riemann ? launch_t<NDIM, 3, 1>(a, S, s) : launch_t<NDIM, 3, 0>(a, S, s);
-    if (recon == 4) return riemann ? launch_t<NDIM, 4, 1>(a, S, s) : launch_t<NDIM, 4, 0>(a, S, s);
-    return riemann ? launch_t<NDIM, 2, 1>(a, S, s) : launch_t<NDIM, 2, 0>(a, S, s);
+    if (recon == 0) return launch_r<NDIM, 0>(a, riemann, S, s);
+    if (recon == 1) return launch_r<NDIM, 1>(a, riemann, S, s);
+    if (recon == 3) return launch_r<NDIM, 3>(a, riemann, S, s);
+    if (recon == 4) return launch_r<NDIM, 4>(a, riemann, S, s);
+    return launch_r<NDIM, 2>(a, riemann, S, s);
 }
 
 }  // namespace

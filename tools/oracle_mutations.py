@@ -53,11 +53,12 @@ MUTATIONS = [
     ("positivity fallback tests rho only",
      "if (!(wl[0] > 0.0) || !(wl[nv - 1] > 0.0) || !(wr[0] > 0.0) || !(wr[nv - 1] > 0.0)) {",
      "if (!(wl[0] > 0.0) || !(wr[0] > 0.0)) {", 0),
-    ("shockDet compression test reversed", "if (!(up - um < 0.0)) return 0;", "if (!(up - um > 0.0)) return 0;", 0),
+    ("shockDet compression test reversed", "if (!(d < 0.0)) return 0;", "if (!(d > 0.0)) return 0;", 0),
+    ("shockDet without the sound-speed dead band",
+     "if (!(d * d * (rm * rp) > 1e-12 * gamma * (a > b ? a : b))) return 0;", "", 0),
     ("shockDet jump relative to max p", "double pmin = pm < pp ? pm : pp;", "double pmin = pm > pp ? pm : pp;", 0),
-    ("shockDet face uses cell i only",
-     "return shock_cell(un[0], un[2], p[0], p[2], thresh) || shock_cell(un[1], un[3], p[1], p[3], thresh);",
-     "return shock_cell(un[0], un[2], p[0], p[2], thresh);", 0),
+    ("shockDet face uses cell i only", "||\n           shock_cell(un[1], un[3], p[1], p[3], rho[1], rho[3], thresh, gamma);",
+     ";", 0),
     ("hybrid picks HLLC at shocks", "? ORS_HLL : ORS_HLLC;", "? ORS_HLLC : ORS_HLL;", 0),
     ("CFL uses sqrt(p/rho)", "double cs = sqrt(c->gamma * w[nv - 1] / w[0]);", "double cs = sqrt(w[nv - 1] / w[0]);", 0),
 ]
