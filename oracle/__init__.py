@@ -64,6 +64,10 @@ class _Cfg(ctypes.Structure):
     ]
 
 
+class _Amr(ctypes.Structure):
+    _fields_ = [("c", _Cfg), ("rlo", ctypes.c_int32 * 3), ("rhi", ctypes.c_int32 * 3)]
+
+
 _lib = None
 
 
@@ -97,6 +101,12 @@ def lib():
             "oracle_step_telescoping": (i32, [P(_Cfg), dp, d, d, d, dp]),
             "oracle_run": (i32, [P(_Cfg), dp, d, i64, dp, P(ctypes.c_long)]),
             "oracle_num_threads": (i32, []),
+            "oracle_amr_check": (i32, [P(_Amr)]),
+            "oracle_amr_leaves": (i32, [P(_Amr), P(ctypes.c_long), P(ctypes.c_long)]),
+            "oracle_amr_fill": (i32, [P(_Amr), dp, dp]),
+            "oracle_amr_dt": (d, [P(_Amr), dp, d, d]),
+            "oracle_amr_step": (i32, [P(_Amr), dp, d, d, d, i32, dp]),
+            "oracle_amr_run": (i32, [P(_Amr), dp, d, i64, dp, P(ctypes.c_long)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -341,3 +351,56 @@ def run(cfg, U, t_end=0.0, max_steps=0, t0=0.0):
 
 def num_threads() -> int:
     return lib().oracle_num_threads()
+
+
+# ------------------------------------------------ NEXT N3: static two-level AMR
+def _amr(cfg, rlo, rhi) -> _Amr:
+    a = _Amr()
+    a.c = _as_cfg(cfg).c()
+    for d in range(3):
+        a.rlo[d] = int(rlo[d])
+        a.rhi[d] = int(rhi[d])
+    return a
+
+
+def amr_leaves(cfg, rlo, rhi):
+    """(coarse leaves, fine leaves) of the refinement of coarse blocks [rlo, rhi)."""
+    a = _amr(cfg, rlo, rhi)
+    nc, nf = ctypes.c_long(), ctypes.c_long()
+    _chk(lib().oracle_amr_leaves(ctypes.byref(a), ctypes.byref(nc), ctypes.byref(nf)), "amr_leaves")
+    return nc.value, nf.value
+
+
+def amr_fill(cfg, rlo, rhi, U) -> np.ndarray:
+    cfg = _as_cfg(cfg)
+    a = _amr(cfg, rlo, rhi)
+    nl = sum(amr_leaves(cfg, rlo, rhi))
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    g = [cfg.ng if d < cfg.ndim else 0 for d in range(3)]
+    P = np.empty((cfg.nvar, nl, cfg.nb[2] + 2 * g[2], cfg.nb[1] + 2 * g[1], cfg.nb[0] + 2 * g[0]))
+    _chk(lib().oracle_amr_fill(ctypes.byref(a), _dp(U), _dp(P)), "amr_fill")
+    return P
+
+
+def amr_dt(cfg, rlo, rhi, U, t=0.0, t_end=0.0) -> float:
+    a = _amr(cfg, rlo, rhi)
+    return lib().oracle_amr_dt(ctypes.byref(a), _dp(np.ascontiguousarray(U, dtype=np.float64)), t, t_end)
+
+
+def amr_step(cfg, rlo, rhi, U, t=0.0, t_end=0.0, dt_fixed=0.0, correct=True):
+    """One composite step (fluxBuff + flux correction); returns (U, dt)."""
+    a = _amr(cfg, rlo, rhi)
+    U = np.array(U, dtype=np.float64, copy=True, order="C")
+    dt = ctypes.c_double()
+    _chk(lib().oracle_amr_step(ctypes.byref(a), _dp(U), t, t_end, dt_fixed, int(correct), ctypes.byref(dt)),
+         "amr_step")
+    return U, dt.value
+
+
+def amr_run(cfg, rlo, rhi, U, t_end=0.0, max_steps=0):
+    a = _amr(cfg, rlo, rhi)
+    U = np.array(U, dtype=np.float64, copy=True, order="C")
+    t, n = ctypes.c_double(0.0), ctypes.c_long(0)
+    _chk(lib().oracle_amr_run(ctypes.byref(a), _dp(U), t_end, max_steps, ctypes.byref(t), ctypes.byref(n)),
+         "amr_run")
+    return U, t.value, n.value

@@ -477,10 +477,42 @@ double oracle_dt(const ocfg* c, const double* U, double t, double t_end) {
  * U_prev is read from the interior of P.  Un may be NULL when a == 0.
  * Returns OERR_NONPHYSICAL if any updated cell has rho <= 0, p <= 0 or a
  * non-finite value (calcEos; reading R12). */
+/* Largest number of cells on one face of a block (face-flux buffers). */
+static long face_cells_max(const ocfg* c) {
+    long m = 1;
+    for (int d = 0; d < c->ndim; d++) {
+        long f = 1;
+        for (int e = 0; e < c->ndim; e++)
+            if (e != d) f *= c->nb[e];
+        if (f > m) m = f;
+    }
+    return m;
+}
+
+/* Cell index on the face of a block normal to d: the two other coordinates,
+ * the lower dimension fastest. */
+static long face_cell(const ocfg* c, int d, int i, int j, int k) {
+    if (d == 0) return (long)k * c->nb[1] + j;
+    if (d == 1) return (long)k * c->nb[0] + i;
+    return (long)j * c->nb[0] + i;
+}
+
+static int stage_padded_fb(const ocfg* c, const double* P, const double* Un, double a, double b, double dt,
+                           double* Uout, double* Fb);
+
+/* One stage on padded blocks (guards already filled). */
 int oracle_stage_padded(const ocfg* c, const double* P, const double* Un, double a, double b, double dt,
                         double* Uout) {
+    return stage_padded_fb(c, P, Un, a, b, dt, Uout, NULL);
+}
+
+/* ... and, when Fb != NULL, the fluxes through each block's 2*ndim faces
+ * (fluxBuff, Alg. 8): Fb[blk][2 d + side][v][face cell], face_cell()
+ * order, face_cells_max() cells per face slot. */
+static int stage_padded_fb(const ocfg* c, const double* P, const double* Un, double a, double b, double dt,
+                           double* Uout, double* Fb) {
     if (oracle_check_config(c)) return OERR_ARG;
-    const int nv = nvar_of(c), ng = c->ng, ndim = c->ndim;
+    const int nv = nvar_of(c), ndim = c->ndim;
     const long NB = nblocks(c), nc = cells_per_block(c), np = padded_cells(c);
     const int g[3] = {guard_of(c, 0), guard_of(c, 1), guard_of(c, 2)};
     const int pn[3] = {c->nb[0] + 2 * g[0], c->nb[1] + 2 * g[1], c->nb[2] + 2 * g[2]};
@@ -531,6 +563,13 @@ int oracle_stage_padded(const ocfg* c, const double* P, const double* Un, double
                             riemann_ax(face_solver(c, ngk, nv, st), nv, c->gamma, ax, wl, wr, fr);
                             long fidx = ((long)k * fn[1] + j) * fn[0] + i;
                             for (int v = 0; v < nv; v++) F[d][(long)rot[v] * nf[d] + fidx] = fr[v];
+                            const int at[3] = {i, j, k};
+                            if (Fb && (at[d] == 0 || at[d] == c->nb[d])) {  /* a face of the block */
+                                const long mf = face_cells_max(c);
+                                const int side = at[d] == 0 ? 0 : 1;
+                                double* fb = Fb + (blk * 6 + 2 * d + side) * nv * mf;
+                                for (int v = 0; v < nv; v++) fb[(long)rot[v] * mf + face_cell(c, d, i, j, k)] = fr[v];
+                            }
                         }
             }
             /* updSoln + calcEos */
@@ -675,10 +714,10 @@ int oracle_step_telescoping(const ocfg* c, double* U, double t, double t_end, do
     if (oracle_check_config(c)) return OERR_ARG;
     const int nv = nvar_of(c), ndim = c->ndim, S = c->rk_stages, ngk = ngk_of(c->recon);
     const int G = S * ngk;
-    ocfg ct = *c;  /* fill with the thick halo */
-    ct.ng = G;
+    /* the per-dimension maps of the thick halo need at least G cells per
+     * dimension (a reflect map of a deeper guard would leave the domain) */
     for (int d = 0; d < ndim; d++)
-        if (c->nb[d] < 1) return OERR_ARG;
+        if ((long)c->nblk[d] * c->nb[d] < G) return OERR_ARG;
     const long NB = nblocks(c), nc = cells_per_block(c);
     int g[3], pn[3];
     long np = 1;
@@ -818,5 +857,428 @@ int oracle_step_telescoping(const ocfg* c, double* U, double t, double t_end, do
     if (st == OK) memcpy(U, Unew, sizeof(double) * nv * NB * nc);
     free(P);
     free(Unew);
+    return st;
+}
+
+/* =========================================================================
+ * NEXT N3: fluxBuff + flux correction on a static two-level refinement, the
+ * all-levels variant (lst:spark-all-levels P:1510-1523;
+ * fluxBuff in Alg. 8).  Plain and slow, like everything above.
+ *
+ * Grid (reading R22): the coarse level is the block grid of
+ * the ocfg; the coarse blocks [rlo, rhi) (per dimension) are refined by 2:
+ * each is replaced by 2^ndim fine blocks of nb cells and spacing dx/2.  The
+ * leaves — coarse blocks outside the box, then fine blocks of the box, each
+ * set lexicographic with x fastest — are updated together with ONE dt
+ * ("all blocks are updated regardless of the levels of refinement", P:1496;
+ * no subcycling).  Canonical leaf state U[v][leaf][k][j][i].
+ *
+ * fill_guardcells at the coarse-fine boundary (reading R22): a face guard
+ * cell is mapped per dimension by the boundary condition at its own level,
+ * then read from the leaf that owns it: same level -> copy; a fine guard in a
+ * coarse leaf -> the value of the coarse cell that contains it (piecewise-
+ * constant prolongation: conservative, exact for uniform states); a coarse
+ * guard over the refined box -> the mean of the 2^ndim fine cells it covers
+ * (restriction).  Means are pairwise sums in a fixed order times 2^-k, exact
+ * for equal values; the children (x fastest) are paired along the diagonals,
+ * ((c00 + c11) + (c10 + c01)) per z layer, so that the result is invariant
+ * under x<->y transposition.  Edge and corner guards are never read (star
+ * stencil).
+ *
+ * fluxBuff (reading R23): every leaf keeps the fluxes through its 2*ndim
+ * faces accumulated over the stages with the Shu-Osher weights of the
+ * stage, B <- b_s (B + F^(s)) (B = 0 before stage 1), so that
+ * U^(n+1) = U^n + dt sum_s c_s L^(s) implies the face's total contribution
+ * is dt * B.  communicate_fluxes + flux correction, once per step after the
+ * last stage: a coarse cell next to a coarse-fine face has its flux replaced
+ * by the area mean of the 2^(ndim-1) fine fluxes through the same face,
+ * U_c += (+1 high face / -1 low face) dt (B_c - mean B_f) / dx_c,
+ * which makes the composite update conservative to round-off.
+ * ========================================================================= */
+typedef struct {
+    ocfg c;                 /* coarse level */
+    int32_t rlo[3], rhi[3]; /* refined coarse blocks, [rlo, rhi) */
+} oamr;
+
+static int amr_refined(const oamr* a, const long* cb) {
+    for (int d = 0; d < 3; d++)
+        if (cb[d] < a->rlo[d] || cb[d] >= a->rhi[d]) return 0;
+    return 1;
+}
+
+static int amr_has_box(const oamr* a) {
+    for (int d = 0; d < 3; d++)
+        if (a->rhi[d] <= a->rlo[d]) return 0;
+    return 1;
+}
+
+static void amr_fine_grid(const oamr* a, long* fnb) {
+    for (int d = 0; d < 3; d++) fnb[d] = d < a->c.ndim ? 2L * (a->rhi[d] - a->rlo[d]) : 1;
+}
+
+int oracle_amr_check(const oamr* a) {
+    const ocfg* c = &a->c;
+    if (oracle_check_config(c)) return OERR_ARG;
+    for (int d = 0; d < 3; d++) {
+        if (a->rlo[d] < 0 || a->rhi[d] > c->nblk[d] || a->rlo[d] > a->rhi[d]) return OERR_ARG;
+        if (d >= c->ndim && amr_has_box(a) && (a->rlo[d] != 0 || a->rhi[d] != 1)) return OERR_ARG;
+        if (d < c->ndim && amr_has_box(a) && c->nb[d] % 2) return OERR_ARG; /* fine cells pair up */
+    }
+    return OK;
+}
+
+int oracle_amr_leaves(const oamr* a, long* ncoarse, long* nfine) {
+    if (oracle_amr_check(a)) return OERR_ARG;
+    long nc = 0;
+    for (long bz = 0; bz < a->c.nblk[2]; bz++)
+        for (long by = 0; by < a->c.nblk[1]; by++)
+            for (long bx = 0; bx < a->c.nblk[0]; bx++) {
+                long cb[3] = {bx, by, bz};
+                if (!(amr_has_box(a) && amr_refined(a, cb))) nc++;
+            }
+    long fnb[3];
+    amr_fine_grid(a, fnb);
+    *ncoarse = nc;
+    *nfine = amr_has_box(a) ? fnb[0] * fnb[1] * fnb[2] : 0;
+    return OK;
+}
+
+/* leaf -> level and block coordinates at that level */
+static void amr_leaf(const oamr* a, long leaf, int* level, long* blk) {
+    long seen = 0;
+    for (long bz = 0; bz < a->c.nblk[2]; bz++)
+        for (long by = 0; by < a->c.nblk[1]; by++)
+            for (long bx = 0; bx < a->c.nblk[0]; bx++) {
+                long cb[3] = {bx, by, bz};
+                if (amr_has_box(a) && amr_refined(a, cb)) continue;
+                if (seen == leaf) {
+                    *level = 0;
+                    blk[0] = bx, blk[1] = by, blk[2] = bz;
+                    return;
+                }
+                seen++;
+            }
+    long f = leaf - seen, fnb[3];
+    amr_fine_grid(a, fnb);
+    *level = 1;
+    blk[0] = 2L * a->rlo[0] + f % fnb[0];
+    blk[1] = (a->c.ndim >= 2 ? 2L * a->rlo[1] : 0) + (f / fnb[0]) % fnb[1];
+    blk[2] = (a->c.ndim >= 3 ? 2L * a->rlo[2] : 0) + f / (fnb[0] * fnb[1]);
+}
+
+/* block coordinates at a level -> leaf index (-1: not a leaf) */
+static long amr_leaf_of(const oamr* a, int level, const long* blk) {
+    long ncl, nfl;
+    oracle_amr_leaves(a, &ncl, &nfl);
+    if (level == 0) {
+        if (amr_has_box(a) && amr_refined(a, blk)) return -1;
+        long seen = 0;
+        for (long bz = 0; bz < a->c.nblk[2]; bz++)
+            for (long by = 0; by < a->c.nblk[1]; by++)
+                for (long bx = 0; bx < a->c.nblk[0]; bx++) {
+                    long cb[3] = {bx, by, bz};
+                    if (amr_has_box(a) && amr_refined(a, cb)) continue;
+                    if (bx == blk[0] && by == blk[1] && bz == blk[2]) return seen;
+                    seen++;
+                }
+        return -1;
+    }
+    long fnb[3], r[3];
+    amr_fine_grid(a, fnb);
+    for (int d = 0; d < 3; d++) {
+        r[d] = blk[d] - (d < a->c.ndim ? 2L * a->rlo[d] : 0);
+        if (r[d] < 0 || r[d] >= fnb[d]) return -1;
+    }
+    return ncl + r[0] + fnb[0] * (r[1] + fnb[1] * r[2]);
+}
+
+/* Level-L cells per dimension. */
+static long amr_ncells(const oamr* a, int level, int d) {
+    long n = (long)a->c.nblk[d] * a->c.nb[d];
+    return d < a->c.ndim ? n << level : n;
+}
+
+/* Conserved value v of the cell with level-L global coordinates g (inside
+ * the domain), from the leaf that owns it (prolongation / restriction as in
+ * the header). */
+static double amr_value(const oamr* a, const double* U, long nleaf, int level, const long* g, int v) {
+    const ocfg* c = &a->c;
+    const long nc = cells_per_block(c);
+    if (level == 1) {
+        long cg[3], cb[3];
+        for (int d = 0; d < 3; d++) {
+            cg[d] = d < c->ndim ? g[d] / 2 : g[d];
+            cb[d] = cg[d] / c->nb[d];
+        }
+        if (!amr_refined(a, cb)) return amr_value(a, U, nleaf, 0, cg, v); /* prolongation: injection */
+        long fb[3], fc[3];
+        for (int d = 0; d < 3; d++) fb[d] = g[d] / c->nb[d], fc[d] = g[d] % c->nb[d];
+        long leaf = amr_leaf_of(a, 1, fb);
+        return U[((long)v * nleaf + leaf) * nc + (fc[2] * c->nb[1] + fc[1]) * c->nb[0] + fc[0]];
+    }
+    long cb[3];
+    for (int d = 0; d < 3; d++) cb[d] = g[d] / c->nb[d];
+    if (!(amr_has_box(a) && amr_refined(a, cb))) {
+        long leaf = amr_leaf_of(a, 0, cb);
+        long lc[3];
+        for (int d = 0; d < 3; d++) lc[d] = g[d] % c->nb[d];
+        return U[((long)v * nleaf + leaf) * nc + (lc[2] * c->nb[1] + lc[1]) * c->nb[0] + lc[0]];
+    }
+    /* restriction: pairwise mean of the 2^ndim fine children, x fastest */
+    double s[8];
+    int n = 1 << c->ndim;
+    for (int q = 0; q < n; q++) {
+        long fg[3] = {g[0], g[1], g[2]};
+        for (int d = 0; d < c->ndim; d++) fg[d] = 2 * g[d] + ((q >> d) & 1);
+        s[q] = amr_value(a, U, nleaf, 1, fg, v);
+    }
+    /* diagonal pairs first: the sum is invariant under x<->y transposition */
+    if (n == 2) return (s[0] + s[1]) * 0.5;
+    if (n == 4) return ((s[0] + s[3]) + (s[1] + s[2])) * 0.25;
+    return (((s[0] + s[3]) + (s[1] + s[2])) + ((s[4] + s[7]) + (s[5] + s[6]))) * 0.125;
+}
+
+/* fill_guardcells for the leaves: P[v][leaf][padded cells] (padded layout of
+ * oracle_fill_guardcells with the leaf list as the blocks); interior copied,
+ * face guards per reading R22, edge/corner guards NaN (never read). */
+int oracle_amr_fill(const oamr* a, const double* U, double* P) {
+    if (oracle_amr_check(a)) return OERR_ARG;
+    const ocfg* c = &a->c;
+    long ncl, nfl;
+    oracle_amr_leaves(a, &ncl, &nfl);
+    const long nleaf = ncl + nfl, np = padded_cells(c);
+    const int nv = nvar_of(c);
+    const int g[3] = {guard_of(c, 0), guard_of(c, 1), guard_of(c, 2)};
+    const int pn[3] = {c->nb[0] + 2 * g[0], c->nb[1] + 2 * g[1], c->nb[2] + 2 * g[2]};
+#pragma omp parallel for schedule(dynamic)
+    for (long leaf = 0; leaf < nleaf; leaf++) {
+        int level;
+        long blk[3];
+        amr_leaf(a, leaf, &level, blk);
+        for (int pk = 0; pk < pn[2]; pk++)
+            for (int pj = 0; pj < pn[1]; pj++)
+                for (int pi = 0; pi < pn[0]; pi++) {
+                    const int loc[3] = {pi - g[0], pj - g[1], pk - g[2]};
+                    int out = 0, dout = -1;
+                    for (int d = 0; d < 3; d++)
+                        if (loc[d] < 0 || loc[d] >= c->nb[d]) out++, dout = d;
+                    const long pidx = ((long)pk * pn[1] + pj) * pn[0] + pi;
+                    if (out > 1) {
+                        for (int v = 0; v < nv; v++) P[((long)v * nleaf + leaf) * np + pidx] = NAN;
+                        continue;
+                    }
+                    long gc[3];
+                    for (int d = 0; d < 3; d++) gc[d] = blk[d] * c->nb[d] + loc[d];
+                    int flip = 0;
+                    if (dout >= 0)
+                        gc[dout] = map_dim(gc[dout], amr_ncells(a, level, dout), c->bc[dout][0], c->bc[dout][1], &flip);
+                    for (int v = 0; v < nv; v++) {
+                        double val = amr_value(a, U, nleaf, level, gc, v);
+                        if (flip && v == 1 + dout) val = -val;
+                        P[((long)v * nleaf + leaf) * np + pidx] = val;
+                    }
+                }
+    }
+    return OK;
+}
+
+/* dt = C min over all leaf cells of min_d dx_L,d / (|u_d| + c)  (reading R7
+ * with each leaf's own spacing), clipped to t_end - t. */
+double oracle_amr_dt(const oamr* a, const double* U, double t, double t_end) {
+    const ocfg* c = &a->c;
+    long ncl, nfl;
+    oracle_amr_leaves(a, &ncl, &nfl);
+    const long nleaf = ncl + nfl, nc = cells_per_block(c);
+    const int nv = nvar_of(c);
+    double best = INFINITY;
+    for (long leaf = 0; leaf < nleaf; leaf++) {
+        const double f = leaf < ncl ? 1.0 : 0.5;
+        for (long q = 0; q < nc; q++) {
+            double u[5], w[5];
+            for (int v = 0; v < nv; v++) u[v] = U[((long)v * nleaf + leaf) * nc + q];
+            cons_to_prim(c->ndim, c->gamma, u, w);
+            double cs = sqrt(c->gamma * w[nv - 1] / w[0]);
+            for (int d = 0; d < c->ndim; d++) {
+                double tt = f * dx_of(c, d) / (fabs(w[1 + d]) + cs);
+                if (tt < best) best = tt;
+            }
+        }
+    }
+    double dt = c->cfl * best;
+    if (t_end > 0.0 && dt > t_end - t) dt = t_end - t;
+    return dt;
+}
+
+/* One stage on every leaf: fill, then the uniform stage per level (each
+ * level's leaves as a block list with that level's spacing); the face fluxes
+ * enter fluxBuff: B <- b (B + F).  B: [leaf][2 d + side][v][face cell],
+ * 6 * nv * face_cells_max per leaf. */
+static int amr_stage(const oamr* a, const double* Uprev, const double* Un, double sa, double sb, double dt,
+                     double* Uout, double* B) {
+    const ocfg* c = &a->c;
+    long ncl, nfl;
+    oracle_amr_leaves(a, &ncl, &nfl);
+    const long nleaf = ncl + nfl, nc = cells_per_block(c), np = padded_cells(c), mf = face_cells_max(c);
+    const int nv = nvar_of(c);
+    double* P = malloc(sizeof(double) * nv * nleaf * np);
+    if (!P) return OERR_OOM;
+    oracle_amr_fill(a, Uprev, P);
+    int st = OK;
+    for (int level = 0; level < 2 && st == OK; level++) {
+        const long l0 = level ? ncl : 0, nl = level ? nfl : ncl;
+        if (nl == 0) continue;
+        ocfg cl = *c;  /* the level's leaves as one block list (along x), the level's spacing */
+        cl.nblk[0] = (int32_t)nl, cl.nblk[1] = 1, cl.nblk[2] = 1;
+        for (int d = 0; d < 3; d++) {
+            const double dxl = dx_of(c, d) * (level ? 0.5 : 1.0);
+            cl.lo[d] = 0.0;
+            cl.hi[d] = d < c->ndim ? dxl * (double)(d == 0 ? nl : 1) * c->nb[d] : c->hi[d] - c->lo[d];
+        }
+        double* Pl = malloc(sizeof(double) * nv * nl * np);
+        double* Ul = malloc(sizeof(double) * nv * nl * nc);
+        double* Ol = malloc(sizeof(double) * nv * nl * nc);
+        double* Fl = malloc(sizeof(double) * nl * 6 * nv * mf);
+        for (int v = 0; v < nv; v++) {
+            memcpy(Pl + (long)v * nl * np, P + ((long)v * nleaf + l0) * np, sizeof(double) * nl * np);
+            memcpy(Ul + (long)v * nl * nc, Un + ((long)v * nleaf + l0) * nc, sizeof(double) * nl * nc);
+        }
+        st = stage_padded_fb(&cl, Pl, Ul, sa, sb, dt, Ol, Fl);
+        for (int v = 0; v < nv; v++)
+            memcpy(Uout + ((long)v * nleaf + l0) * nc, Ol + (long)v * nl * nc, sizeof(double) * nl * nc);
+        for (long q = 0; q < nl * 6 * nv * mf; q++) {
+            double* bq = B + l0 * 6 * nv * mf + q;
+            *bq = sb * (*bq + Fl[q]);
+        }
+        free(Pl), free(Ul), free(Ol), free(Fl);
+    }
+    free(P);
+    return st;
+}
+
+/* communicate_fluxes + flux correction (lst:spark-all-levels): every coarse
+ * cell next to a coarse-fine face.  Returns OERR_NONPHYSICAL if a corrected
+ * cell has rho <= 0, p <= 0 or a non-finite value. */
+static int amr_fluxcorr(const oamr* a, const double* B, double dt, double* U) {
+    const ocfg* c = &a->c;
+    if (!amr_has_box(a)) return OK;
+    long ncl, nfl;
+    oracle_amr_leaves(a, &ncl, &nfl);
+    const long nleaf = ncl + nfl, nc = cells_per_block(c), mf = face_cells_max(c);
+    const int nv = nvar_of(c), ndim = c->ndim;
+    int bad = 0;
+    for (long leaf = 0; leaf < ncl; leaf++) {
+        int level;
+        long blk[3];
+        amr_leaf(a, leaf, &level, blk);
+        for (int d = 0; d < ndim; d++)
+            for (int side = 0; side < 2; side++) {
+                /* the coarse block across the face (boundary map at the coarse level) */
+                long nb_[3] = {blk[0], blk[1], blk[2]};
+                long gface = side ? (blk[d] + 1) * c->nb[d] : blk[d] * c->nb[d] - 1;  /* coarse cell across */
+                int flip;
+                long gm = map_dim(gface, amr_ncells(a, 0, d), c->bc[d][0], c->bc[d][1], &flip);
+                if (c->bc[d][side] != OBC_PERIODIC && (gface < 0 || gface >= amr_ncells(a, 0, d))) continue;
+                nb_[d] = gm / c->nb[d];
+                if (!amr_refined(a, nb_)) continue;
+                /* fine cells across the face: level-1 coordinate along d */
+                const long fd = side ? 2 * gm : 2 * gm + 1;
+                const int e1 = d == 0 ? 1 : 0, e2 = d == 2 ? 1 : 2;  /* transverse dims, increasing */
+                const int n1 = ndim > 1 ? c->nb[e1] : 1, n2 = ndim > 2 ? c->nb[e2] : 1;
+                for (int t2 = 0; t2 < n2; t2++)
+                    for (int t1 = 0; t1 < n1; t1++) {
+                        int lc[3];
+                        lc[d] = side ? c->nb[d] - 1 : 0;
+                        lc[e1] = t1;
+                        lc[e2] = t2;
+                        if (ndim < 3) lc[2] = 0;
+                        if (ndim < 2) lc[1] = 0;
+                        const long cell = ((long)lc[2] * c->nb[1] + lc[1]) * c->nb[0] + lc[0];
+                        const long fcl = face_cell(c, d, lc[0], lc[1], lc[2]);
+                        /* the 2^(ndim-1) fine faces: transverse fine coordinates, e1 fastest */
+                        double fsum[5] = {0, 0, 0, 0, 0};
+                        for (int v = 0; v < nv; v++) {
+                            double s4[4];
+                            int nf = 1 << (ndim - 1);
+                            for (int q = 0; q < nf; q++) {
+                                long fg[3];
+                                fg[d] = fd;
+                                fg[e1] = 2 * (blk[e1] * c->nb[e1] + t1) + (ndim > 1 ? (q & 1) : 0);
+                                fg[e2] = 2 * (blk[e2] * c->nb[e2] + t2) + (ndim > 2 ? ((q >> 1) & 1) : 0);
+                                if (ndim < 3) fg[2] = 0;
+                                if (ndim < 2) fg[1] = 0;
+                                long fb[3], fl[3];
+                                for (int e = 0; e < 3; e++) fb[e] = fg[e] / c->nb[e], fl[e] = fg[e] % c->nb[e];
+                                const long fleaf = amr_leaf_of(a, 1, fb);
+                                const long ffc = face_cell(c, d, (int)fl[0], (int)fl[1], (int)fl[2]);
+                                s4[q] = B[((fleaf * 6 + 2 * d + (1 - side)) * nv + v) * mf + ffc];
+                            }
+                            if (nf == 1) fsum[v] = s4[0];
+                            else if (nf == 2) fsum[v] = (s4[0] + s4[1]) * 0.5;
+                            else fsum[v] = ((s4[0] + s4[3]) + (s4[1] + s4[2])) * 0.25;  /* diagonal pairs */
+                        }
+                        double u[5], w[5];
+                        for (int v = 0; v < nv; v++) {
+                            const double bc_ = B[((leaf * 6 + 2 * d + side) * nv + v) * mf + fcl];
+                            const double corr = dt * (bc_ - fsum[v]) / dx_of(c, d);
+                            double* uq = U + ((long)v * nleaf + leaf) * nc + cell;
+                            *uq = side ? *uq + corr : *uq - corr;
+                            u[v] = *uq;
+                        }
+                        cons_to_prim(ndim, c->gamma, u, w);
+                        int ok = w[0] > 0.0 && w[nv - 1] > 0.0;
+                        for (int v = 0; v < nv; v++) ok = ok && isfinite(u[v]);
+                        if (!ok) bad = 1;
+                    }
+            }
+    }
+    return bad ? OERR_NONPHYSICAL : OK;
+}
+
+/* One SSP-RK step of the composite grid (all-levels variant): dt from every
+ * leaf, the S stages with fluxBuff, then communicate_fluxes + correction.
+ * correct = 0 skips the correction (for the pin that shows it is needed).
+ * On failure U is unchanged. */
+int oracle_amr_step(const oamr* a, double* U, double t, double t_end, double dt_fixed, int correct, double* dt_used) {
+    if (oracle_amr_check(a)) return OERR_ARG;
+    const ocfg* c = &a->c;
+    long ncl, nfl;
+    oracle_amr_leaves(a, &ncl, &nfl);
+    const long nleaf = ncl + nfl, n = (long)nvar_of(c) * nleaf * cells_per_block(c);
+    const long nb_ = nleaf * 6 * nvar_of(c) * face_cells_max(c);
+    double dt = dt_fixed > 0.0 ? dt_fixed : oracle_amr_dt(a, U, t, t_end);
+    if (dt_used) *dt_used = dt;
+    double* S0 = malloc(sizeof(double) * n);
+    double* S1 = malloc(sizeof(double) * n);
+    double* B = calloc(nb_, sizeof(double));
+    if (!S0 || !S1 || !B) { free(S0), free(S1), free(B); return OERR_OOM; }
+    const double* prev = U;
+    double* bufs[2] = {S0, S1};
+    int st = OK;
+    for (int s = 1; s <= c->rk_stages && st == OK; s++) {
+        double sa, sb;
+        oracle_rk_coeffs(c->rk_stages, s, &sa, &sb);
+        double* out = bufs[(s - 1) & 1];
+        st = amr_stage(a, prev, U, sa, sb, dt, out, B);
+        prev = out;
+    }
+    double* res = (double*)prev;
+    if (st == OK && correct) st = amr_fluxcorr(a, B, dt, res);
+    if (st == OK) memcpy(U, res, sizeof(double) * n);
+    free(S0), free(S1), free(B);
+    return st;
+}
+
+int oracle_amr_run(const oamr* a, double* U, double t_end, long max_steps, double* t, long* nsteps) {
+    int st = OK;
+    while (st == OK) {
+        if (t_end > 0.0 && *t >= t_end * (1.0 - 1e-14)) break;
+        if (max_steps > 0 && *nsteps >= max_steps) break;
+        double dt;
+        st = oracle_amr_step(a, U, *t, t_end, 0.0, 1, &dt);
+        if (st == OK) {
+            *t += dt;
+            *nsteps += 1;
+        }
+    }
     return st;
 }

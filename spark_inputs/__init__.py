@@ -325,3 +325,85 @@ def initial_primitive(p: Problem, seed: int = 0, box=None) -> np.ndarray:
     if p.ic == "blocky":
         return random_state(p, seed, blocky=True)
     raise ValueError(p.ic)
+
+
+# ------------------------------------------ NEXT N3: static two-level refinement
+# Layout only (no method arithmetic): the leaf list of a refinement of the
+# coarse blocks [rlo, rhi) by 2 — coarse blocks outside the box, then the fine
+# blocks of the box, each lexicographic with x fastest — and primitive states
+# evaluated at the leaves' cell centres.  Leaf states are [v][leaf][k][j][i].
+def amr_leaf_blocks(p: Problem, rlo, rhi):
+    """[(level, (bx, by, bz))] in leaf order (fine block coordinates are on the
+    global fine block grid)."""
+    has_box = all(rhi[d] > rlo[d] for d in range(3))
+    out = []
+    for bz in range(p.nblk[2]):
+        for by in range(p.nblk[1]):
+            for bx in range(p.nblk[0]):
+                inside = has_box and all(rlo[d] <= b < rhi[d] for d, b in enumerate((bx, by, bz)))
+                if not inside:
+                    out.append((0, (bx, by, bz)))
+    if has_box:
+        f = [2 * (rhi[d] - rlo[d]) if d < p.ndim else 1 for d in range(3)]
+        o = [2 * rlo[d] if d < p.ndim else 0 for d in range(3)]
+        for bz in range(f[2]):
+            for by in range(f[1]):
+                for bx in range(f[0]):
+                    out.append((1, (o[0] + bx, o[1] + by, o[2] + bz)))
+    return out
+
+
+def amr_centres(p: Problem, rlo, rhi):
+    """Cell centres (x, y, z) of every leaf cell, arrays [leaf][k][j][i], and
+    the cell spacing factor of each leaf (1 coarse, 1/2 fine)."""
+    leaves = amr_leaf_blocks(p, rlo, rhi)
+    dx = [(p.hi[d] - p.lo[d]) / (p.nblk[d] * p.nb[d]) for d in range(3)]
+    X = np.zeros((3, len(leaves), p.nb[2], p.nb[1], p.nb[0]))
+    fac = np.ones(len(leaves))
+    for q, (lev, b) in enumerate(leaves):
+        f = 0.5 if lev else 1.0
+        fac[q] = f
+        for d in range(3):
+            h = dx[d] * (f if d < p.ndim else 1.0)
+            c = p.lo[d] + (b[d] * p.nb[d] + np.arange(p.nb[d]) + 0.5) * h
+            shape = [1, 1, 1]
+            shape[2 - d] = p.nb[d]
+            X[d, q] = c.reshape(shape)
+    return X[0], X[1], X[2], fac
+
+
+def amr_primitive(p: Problem, rlo, rhi, kind: str, seed: int = 0) -> np.ndarray:
+    """Primitive leaf state W[v][leaf][k][j][i]:
+    'random'  rho, p ~ U[0.5, 1.5], u ~ U[-0.5, 0.5] per cell (seeded);
+    'uniform' one random constant state;
+    'pulse'   rho = 1 + 0.5 g, p = 1 + 2 g, u_d = 0.3 (d+1)/ndim,
+              g = exp(-|x - x0|^2 / 0.01), x0 = 0.4 per dim (crosses the box);
+    'sod_x'   Toro Test 1 along x (x < 0.5 left state)."""
+    x, y, z, _ = amr_centres(p, rlo, rhi)
+    nl = x.shape[0]
+    W = np.zeros((p.nvar,) + x.shape)
+    g = np.random.Generator(np.random.PCG64(seed))
+    if kind == "random":
+        W[0] = g.uniform(0.5, 1.5, x.shape)
+        for d in range(p.ndim):
+            W[1 + d] = g.uniform(-0.5, 0.5, x.shape)
+        W[-1] = g.uniform(0.5, 1.5, x.shape)
+    elif kind == "uniform":
+        W[0] = g.uniform(0.5, 1.5)
+        for d in range(p.ndim):
+            W[1 + d] = g.uniform(-0.5, 0.5)
+        W[-1] = g.uniform(0.5, 1.5)
+    elif kind == "pulse":
+        r2 = (x - 0.4) ** 2 + ((y - 0.4) ** 2 if p.ndim > 1 else 0.0) + ((z - 0.4) ** 2 if p.ndim > 2 else 0.0)
+        gg = np.exp(-r2 / 0.01)
+        W[0] = 1.0 + 0.5 * gg
+        for d in range(p.ndim):
+            W[1 + d] = 0.3 * (d + 1) / p.ndim
+        W[-1] = 1.0 + 2.0 * gg
+    elif kind == "sod_x":
+        W[0] = np.where(x < 0.5, 1.0, 0.125)
+        W[-1] = np.where(x < 0.5, 1.0, 0.1)
+    else:
+        raise ValueError(kind)
+    assert W.shape[1] == nl
+    return W

@@ -69,7 +69,8 @@ def test_boundary_differences_confined(p):
 
 
 def test_uniform_state_telescoping():
-    p = si.Problem("u", 3, (4, 4, 4), (2, 2, 2), 3, 2, 1, 3, 0.3, bc=((1, 1), (2, 2), (0, 0)))
+    # 12 cells per dimension >= the 9-cell telescoped halo (the oracle refuses less)
+    p = si.Problem("u", 3, (4, 4, 4), (3, 3, 3), 3, 2, 1, 3, 0.3, bc=((1, 1), (2, 2), (0, 0)))
     W = si.uniform_state(p, 2)
     W[1:4] = 0.0  # at rest: reflect walls keep it uniform too
     U0 = cons(p, W)
@@ -99,3 +100,11 @@ def test_sod_telescoping_vs_exact():
     h = 1 / 256
     sel = (x > contact + 4 * h) & (x < shock - 4 * h)
     assert abs(W[0, sel].mean() - rr) < 0.01 * rr
+
+
+def test_halo_deeper_than_domain_refused():
+    """S*NGK guard layers need that many cells per dimension (a reflect map of
+    a deeper guard would leave the domain); the GPU refuses the same case."""
+    p = si.Problem("d", 3, (4, 4, 4), (2, 2, 2), 3, 2, 1, 3, 0.3, bc=((1, 1), (2, 2), (0, 0)))
+    with pytest.raises(oracle.OracleError):
+        oracle.step_telescoping(p.config(), cons(p, si.uniform_state(p, 2)))

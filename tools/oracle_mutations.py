@@ -60,6 +60,15 @@ MUTATIONS = [
     ("shockDet face uses cell i only", "||\n           shock_cell(un[1], un[3], p[1], p[3], rho[1], rho[3], thresh, gamma);",
      ";", 0),
     ("hybrid picks HLLC at shocks", "? ORS_HLL : ORS_HLLC;", "? ORS_HLLC : ORS_HLL;", 0),
+    ("AMR correction sign flipped", "*uq = side ? *uq + corr : *uq - corr;", "*uq = side ? *uq - corr : *uq + corr;", 0),
+    ("AMR fluxBuff without the stage weight", "*bq = sb * (*bq + Fl[q]);", "*bq = *bq + Fl[q];", 0),
+    ("AMR restriction takes one child", "if (n == 4) return ((s[0] + s[3]) + (s[1] + s[2])) * 0.25;",
+     "if (n == 4) return s[0];", 0),
+    ("AMR prolongation from the neighbour coarse cell", "cg[d] = d < c->ndim ? g[d] / 2 : g[d];",
+     "cg[d] = d < c->ndim ? (g[d] + 1) / 2 : g[d];", 0),
+    ("AMR face mean uses one fine face", "else if (nf == 2) fsum[v] = (s4[0] + s4[1]) * 0.5;",
+     "else if (nf == 2) fsum[v] = s4[0];", 0),
+    ("AMR fine dt spacing not halved", "const double f = leaf < ncl ? 1.0 : 0.5;", "const double f = 1.0;", 0),
     ("CFL uses sqrt(p/rho)", "double cs = sqrt(c->gamma * w[nv - 1] / w[0]);", "double cs = sqrt(w[nv - 1] / w[0]);", 0),
 ]
 
