@@ -301,6 +301,44 @@ spark_status spark_axpy(int32_t device, int32_t variant, int64_t n, double a, co
 spark_status spark_selftest_riemann(int32_t device, int32_t riemann, int32_t ndim, int32_t dir, double gamma,
                                     int64_t n, const double* wl, const double* wr, double* f);
 
+/* ---- NEXT N3: fluxBuff + flux correction on a static two-level refinement -------- */
+/* The all-levels variant of PAPER.md P:1494-1506 (lst:spark-all-levels
+ * P:1510-1523; fluxBuff in Alg. 8), readings R22/R23 of DESIGN.md.
+ * The coarse blocks [rlo, rhi) of cfg's block grid are refined by 2 (2^ndim
+ * fine blocks of nb cells, spacing dx/2 each).  Leaves: the coarse blocks
+ * outside the box, then the fine blocks of the box, each lexicographic with x
+ * fastest; the state is U[v][leaf][k][j][i] (canonical layout, leaves as the
+ * blocks).  One dt for all leaves (no subcycling).  Guard cells across a
+ * coarse-fine face: prolongation = the containing coarse cell, restriction =
+ * the mean of the 2^ndim fine cells; each leaf accumulates its face fluxes
+ * over the stages (fluxBuff, B <- b_s (B + F)); after the last stage the
+ * coarse cells on a coarse-fine face take the mean of the fine fluxes
+ * (communicate_fluxes + correction), which makes the step conservative.
+ * Single GPU; nb even along refined dims; no gravity.  Errors as spark_step. */
+typedef struct {
+    int32_t rlo[3], rhi[3];  /* refined coarse blocks [rlo, rhi); rlo == rhi: none */
+} spark_refine;
+
+typedef struct spark_amr spark_amr;
+
+spark_status spark_amr_leaves(const spark_config* cfg, const spark_refine* ref, int64_t* ncoarse, int64_t* nfine);
+spark_status spark_amr_required_bytes(const spark_config* cfg, const spark_refine* ref, size_t* bytes);
+/* arena: device memory of >= required bytes (256-byte aligned), caller-owned. */
+spark_status spark_amr_init(const spark_config* cfg, const spark_refine* ref, int32_t device, void* cuda_stream,
+                            void* arena, size_t arena_bytes, spark_amr** out);
+spark_status spark_amr_finalize(spark_amr* amr);
+const char* spark_amr_last_error(const spark_amr* amr);
+/* Load U[v][leaf][cells] (host or device); resets t and the step count. */
+spark_status spark_amr_set_state(spark_amr* amr, const double* U, int32_t on_device);
+/* Copy U^n out; synchronises; SPARK_ERR_NONPHYSICAL if the failure word is set. */
+spark_status spark_amr_get_state(spark_amr* amr, double* U, int32_t on_device);
+/* Materialise the padded leaves P[v][leaf][padded cells] (device pointer) of
+ * U^n with the coarse-fine guard rules; edge/corner guards NaN.  Asynchronous. */
+spark_status spark_amr_fill_guardcells(spark_amr* amr, double* padded_out);
+/* One composite SSP-RK step (dt / t_end / dt_used as spark_step). */
+spark_status spark_amr_step(spark_amr* amr, double dt, double t_end, double* dt_used);
+spark_status spark_amr_get_time(spark_amr* amr, double* t, int64_t* steps, double* dt_last);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,920 @@
+// spark_amr.cu — NEXT N3: fluxBuff + flux correction on a static two-level
+// refinement, the all-levels variant (lst:spark-all-levels
+// P:1510-1523; fluxBuff in Alg. 8).  Readings R22/R23.
+//
+// The coarse block grid of a spark_config has the coarse blocks [rlo, rhi)
+// replaced by 2^ndim fine blocks each (spacing dx/2).  Leaves = coarse blocks
+// outside the box, then fine blocks of the box (each lexicographic, x
+// fastest); state U[v][leaf][k][j][i] (the ABI's canonical layout with the
+// leaf list as the blocks).  All leaves advance with one dt (no subcycling).
+//
+// Per stage (lst:spark-nontelescoping body, with the coarse-fine guard rules):
+//   KA amr_interior / amr_guard  padded primitive tiles W[v][leaf][padded]:
+//        interior cells converted in place; face guards gathered through a
+//        host-built map (same-level copy, piecewise-constant prolongation,
+//        diagonal-pairwise restriction mean; reflect flips the momentum)
+//   KB amr_face    every face of every leaf: calcLims + calcFlux (the
+//        product's device reconstruction / Riemann / shockDet) -> F; the
+//        leaf-boundary faces also enter fluxBuff, B <- b_s (B + F)
+//   KC amr_update  updSoln: U^(s) = a U^n + b (U^(s-1) + dt L)
+// Per step after the last stage: communicate_fluxes + correction (KD
+// amr_corr, one launch per direction so no two threads touch one cell),
+// then the CFL minimum of the corrected state (KE amr_cfl) for the next dt.
+//
+// This path is built for parity and measurement of the N3 row, not fused like
+// KB1: the padded tiles and the face fluxes go through HBM.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/spark.h"
+#include "spark_device.cuh"
+#include "spark_internal.h"
+
+namespace spark {
+namespace {
+
+using namespace dev;
+
+struct AmrGeo {
+    int ndim, nv, ng, ngk, recon;
+    int nb[3], pn[3];
+    long long nleaf, ncl, nc, np;
+    long long nfd[3], Fo[3], NF;  // faces per leaf per direction, offsets, total
+    long long mf;                 // fluxBuff cells per face slot
+    double rdx[2][3];             // 1/dx per level
+    double gamma, cfl, shock_thresh;
+};
+
+struct GuardE {
+    long long dst;  // leaf * np + padded index
+    long long src;  // leaf * nc + cell (first child for a restriction)
+    int kind;       // 1 copy, 2 restriction; bits 4+d: negate momentum d (reflect)
+    int pad;
+};
+
+struct CorrE {
+    long long cell;   // coarse leaf * nc + cell
+    long long bc;     // (leaf * 6 + slot) * mf + face cell of the coarse side
+    long long bf[4];  // the fine faces (same encoding), 2^(ndim-1) of them
+    int side;         // 1: interface on the coarse cell's high face
+    int pad;
+};
+
+__host__ __device__ inline long long face_cell(const AmrGeo& g, int d, int i, int j, int k) {
+    if (d == 0) return (long long)k * g.nb[1] + j;
+    if (d == 1) return (long long)k * g.nb[0] + i;
+    return (long long)j * g.nb[0] + i;
+}
+
+// ---------------------------------------------------------------- KA
+template <int NV>
+__global__ void amr_interior_kernel(const AmrGeo g, const double* __restrict__ u, double* __restrict__ w,
+                                    int to_prim, DevScalars* sc) {
+    const long long vs = g.nleaf * g.nc, vp = g.nleaf * g.np;
+    const int gx = g.ng, gy = g.ndim >= 2 ? g.ng : 0, gz = g.ndim >= 3 ? g.ng : 0;
+    bool ok = true;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < vs;
+         q += (long long)gridDim.x * blockDim.x) {
+        const long long leaf = q / g.nc, c = q - leaf * g.nc;
+        const int i = (int)(c % g.nb[0]), j = (int)((c / g.nb[0]) % g.nb[1]), k = (int)(c / ((long long)g.nb[0] * g.nb[1]));
+        const long long p = leaf * g.np + ((long long)(k + gz) * g.pn[1] + (j + gy)) * g.pn[0] + (i + gx);
+        double uu[NV], ww[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) uu[v] = u[v * vs + q];
+        if (to_prim) ok &= cons_to_prim<NV>(uu, ww, g.gamma - 1.0);
+#pragma unroll
+        for (int v = 0; v < NV; v++) w[v * vp + p] = to_prim ? ww[v] : uu[v];
+    }
+    if (!ok) flag_nonphysical(sc);
+}
+
+template <int NV>
+__global__ void amr_guard_kernel(const AmrGeo g, const double* __restrict__ u, const GuardE* __restrict__ ge,
+                                 long long n, double* __restrict__ w, int to_prim, DevScalars* sc) {
+    const long long vs = g.nleaf * g.nc, vp = g.nleaf * g.np;
+    const long long ox = 1, oy = g.nb[0], oz = (long long)g.nb[0] * g.nb[1];
+    bool ok = true;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
+        const GuardE E = ge[e];
+        double uu[NV], ww[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) {
+            const double* s = u + v * vs + E.src;
+            double val;
+            if ((E.kind & 15) == 1) {
+                val = s[0];
+            } else if (NV == 3) {  // restriction: diagonal-pairwise mean (reading R22)
+                val = (s[0] + s[ox]) * 0.5;
+            } else if (NV == 4) {
+                val = ((s[0] + s[ox + oy]) + (s[ox] + s[oy])) * 0.25;
+            } else {
+                val = (((s[0] + s[ox + oy]) + (s[ox] + s[oy])) +
+                       ((s[oz] + s[oz + ox + oy]) + (s[oz + ox] + s[oz + oy]))) * 0.125;
+            }
+            if (v >= 1 && v < NV - 1 && ((E.kind >> (3 + v)) & 1)) val = -val;
+            uu[v] = val;
+        }
+        if (to_prim) ok &= cons_to_prim<NV>(uu, ww, g.gamma - 1.0);
+#pragma unroll
+        for (int v = 0; v < NV; v++) w[v * vp + E.dst] = to_prim ? ww[v] : uu[v];
+    }
+    if (!ok) flag_nonphysical(sc);
+}
+
+// ---------------------------------------------------------------- KB
+template <int RECON>
+__device__ __forceinline__ void recon_face(const double* s, double& wl, double& wr) {
+    // s[0..2NGK-1] = W_{i-NGK+1..i+NGK}: wl = hi edge of cell i, wr = lo edge of cell i+1
+    constexpr int R = StencilOf<RECON>::NG - 1;
+    constexpr int K = StencilOf<RECON>::NG;
+    double lo, hi;
+    recon_cell<RECON>(s + (K - 1 - R), lo, hi);
+    wl = hi;
+    recon_cell<RECON>(s + (K - R), lo, hi);
+    wr = lo;
+}
+
+template <int NV, int RS, int D, int RECON>
+__device__ __forceinline__ void amr_face_solve(const AmrGeo& g, const double* __restrict__ w, long long right,
+                                               long long stride, double* f) {
+    constexpr int K = StencilOf<RECON>::NG;
+    const long long vp = g.nleaf * g.np;
+    double wl[NV], wr[NV];
+#pragma unroll
+    for (int v = 0; v < NV; v++) {
+        double s[6];
+#pragma unroll
+        for (int m = 0; m < 2 * K; m++) s[m] = w[v * vp + right + (m - K) * stride];
+        recon_face<RECON>(s, wl[v], wr[v]);
+    }
+    if (RECON != 0 && !(positive(wl[0]) && positive(wl[NV - 1]) && positive(wr[0]) && positive(wr[NV - 1]))) {
+#pragma unroll
+        for (int v = 0; v < NV; v++) {
+            wl[v] = w[v * vp + right - stride];
+            wr[v] = w[v * vp + right];
+        }
+    }
+    bool shk = false;
+    if constexpr (RS == 2) {
+        double uu[4], pp[4], rr[4];
+#pragma unroll
+        for (int m = 0; m < 4; m++) {
+            const long long q = right + (m - 2) * stride;
+            uu[m] = w[(1 + D) * vp + q];
+            pp[m] = w[(NV - 1) * vp + q];
+            rr[m] = w[q];
+        }
+        shk = shock_face(uu, pp, rr, g.shock_thresh, g.gamma);
+    }
+    face_flux<NV, RS, D>(wl, wr, shk, g.gamma, 1.0 / (g.gamma - 1.0), f);
+}
+
+template <int NDIM, int RS>
+__global__ void amr_face_kernel(const AmrGeo g, const double* __restrict__ w, double* __restrict__ F,
+                                double* __restrict__ B, double bco) {
+    constexpr int NV = NDIM + 2;
+    const long long total = g.nleaf * g.NF;
+    const long long fvs = g.nleaf * g.NF, bvs = g.nleaf * 6 * g.mf;
+    const int gx = g.ng, gy = NDIM >= 2 ? g.ng : 0, gz = NDIM >= 3 ? g.ng : 0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long leaf = e / g.NF;
+        long long r = e - leaf * g.NF;
+        const int d = r < g.Fo[1] ? 0 : (r < g.Fo[2] ? 1 : 2);
+        r -= g.Fo[d];
+        int fn[3] = {g.nb[0], g.nb[1], g.nb[2]};
+        fn[d] += 1;
+        const int i = (int)(r % fn[0]), j = (int)((r / fn[0]) % fn[1]), k = (int)(r / ((long long)fn[0] * fn[1]));
+        const long long right = leaf * g.np + ((long long)(k + gz) * g.pn[1] + (j + gy)) * g.pn[0] + (i + gx);
+        const long long stride = d == 0 ? 1 : (d == 1 ? g.pn[0] : (long long)g.pn[0] * g.pn[1]);
+        double f[NV];
+#define AMR_SOLVE(DD)                                                                                    \
+    switch (g.recon) {                                                                                   \
+        case 0: amr_face_solve<NV, RS == 2 ? 1 : RS, DD, 0>(g, w, right, stride, f); break;             \
+        case 1: amr_face_solve<NV, RS, DD, 1>(g, w, right, stride, f); break;                           \
+        case 3: amr_face_solve<NV, RS, DD, 3>(g, w, right, stride, f); break;                           \
+        case 4: amr_face_solve<NV, RS, DD, 4>(g, w, right, stride, f); break;                           \
+        default: amr_face_solve<NV, RS, DD, 2>(g, w, right, stride, f); break;                          \
+    }
+        if (d == 0) {
+            AMR_SOLVE(0)
+        } else if (NDIM >= 2 && d == 1) {
+            AMR_SOLVE((NDIM >= 2 ? 1 : 0))
+        } else if (NDIM >= 3) {
+            AMR_SOLVE((NDIM >= 3 ? 2 : 0))
+        }
+#undef AMR_SOLVE
+#pragma unroll
+        for (int v = 0; v < NV; v++) F[v * fvs + e] = f[v];
+        const int at[3] = {i, j, k};
+        if (at[d] == 0 || at[d] == g.nb[d]) {  // a face of the leaf: fluxBuff (reading R23)
+            const int slot = 2 * d + (at[d] == 0 ? 0 : 1);
+            const long long bi = (leaf * 6 + slot) * g.mf + face_cell(g, d, i, j, k);
+#pragma unroll
+            for (int v = 0; v < NV; v++) B[v * bvs + bi] = bco * (B[v * bvs + bi] + f[v]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- KC
+template <int NDIM>
+__global__ void amr_update_kernel(const AmrGeo g, const double* __restrict__ F, const double* __restrict__ uprev,
+                                  const double* __restrict__ un, double* __restrict__ uout, double a, double b,
+                                  const DevScalars* __restrict__ sc) {
+    constexpr int NV = NDIM + 2;
+    const long long vs = g.nleaf * g.nc, fvs = g.nleaf * g.NF;
+    const double dt = sc->dt;
+    if (!sc->active) {  // t >= t_end or frozen after a failure: U^(s) = U^(s-1)
+        for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < vs * NV;
+             q += (long long)gridDim.x * blockDim.x)
+            uout[q] = uprev[q];
+        return;
+    }
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < vs;
+         q += (long long)gridDim.x * blockDim.x) {
+        const long long leaf = q / g.nc, c = q - leaf * g.nc;
+        const int i = (int)(c % g.nb[0]), j = (int)((c / g.nb[0]) % g.nb[1]), k = (int)(c / ((long long)g.nb[0] * g.nb[1]));
+        const int lev = leaf < g.ncl ? 0 : 1;
+        long long lo[3], hi[3];
+#pragma unroll
+        for (int d = 0; d < NDIM; d++) {
+            int fn[3] = {g.nb[0], g.nb[1], g.nb[2]};
+            fn[d] += 1;
+            const int at[3] = {i, j, k};
+            int up[3] = {i, j, k};
+            up[d] = at[d] + 1;
+            lo[d] = leaf * g.NF + g.Fo[d] + ((long long)k * fn[1] + j) * fn[0] + i;
+            hi[d] = leaf * g.NF + g.Fo[d] + ((long long)up[2] * fn[1] + up[1]) * fn[0] + up[0];
+        }
+#pragma unroll
+        for (int v = 0; v < NV; v++) {
+            const double dfx = (F[v * fvs + hi[0]] - F[v * fvs + lo[0]]) * g.rdx[lev][0];
+            double Lv;
+            if (NDIM == 1) {
+                Lv = -dfx;
+            } else {
+                const double dfy = (F[v * fvs + hi[1]] - F[v * fvs + lo[1]]) * g.rdx[lev][1];
+                if (NDIM == 2) Lv = -(dfx + dfy);
+                else Lv = -(dfx + dfy) - (F[v * fvs + hi[2]] - F[v * fvs + lo[2]]) * g.rdx[lev][2];
+            }
+            const double u0 = uprev[v * vs + q];
+            const double unn = a != 0.0 ? un[v * vs + q] : 0.0;
+            uout[v * vs + q] = fma(b, fma(dt, Lv, u0), a * unn);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- KD
+template <int NV>
+__global__ void amr_corr_kernel(const AmrGeo g, const CorrE* __restrict__ ce, long long n, int d,
+                                const double* __restrict__ B, double* __restrict__ u, const double* __restrict__ dtp,
+                                DevScalars* sc) {
+    const long long vs = g.nleaf * g.nc, bvs = g.nleaf * 6 * g.mf;
+    const double dt = *dtp;
+    bool ok = true;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
+        const CorrE E = ce[e];
+        double uu[NV], ww[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) {
+            const double* bv = B + v * bvs;
+            double m;
+            if (NV == 3) m = bv[E.bf[0]];
+            else if (NV == 4) m = (bv[E.bf[0]] + bv[E.bf[1]]) * 0.5;
+            else m = ((bv[E.bf[0]] + bv[E.bf[3]]) + (bv[E.bf[1]] + bv[E.bf[2]])) * 0.25;  // diagonal pairs
+            const double corr = dt * (bv[E.bc] - m) * g.rdx[0][d];
+            double* uq = u + v * vs + E.cell;
+            const double val = E.side ? *uq + corr : *uq - corr;
+            *uq = val;
+            uu[v] = val;
+        }
+        ok &= cons_to_prim<NV>(uu, ww, g.gamma - 1.0);
+    }
+    if (!ok) flag_nonphysical(sc);
+}
+
+// ---------------------------------------------------------------- KE
+template <int NDIM>
+__global__ void amr_cfl_kernel(const AmrGeo g, const double* __restrict__ u, DevScalars* sc) {
+    constexpr int NV = NDIM + 2;
+    __shared__ double red[32];
+    const long long vs = g.nleaf * g.nc;
+    double mn = INFINITY;
+    bool ok = true;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < vs;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int lev = q / g.nc < g.ncl ? 0 : 1;
+        double uu[NV], ww[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) uu[v] = u[v * vs + q];
+        ok &= cons_to_prim<NV>(uu, ww, g.gamma - 1.0);
+        // reading R7 with the leaf's own spacing: 1 / max_d (|u_d| + c) / dx_d
+        const double gp = g.gamma * ww[NV - 1];
+        const double c = gp * rsqrt_fast(gp * ww[0]);
+        double m = (fabs(ww[1]) + c) * g.rdx[lev][0];
+#pragma unroll
+        for (int d = 1; d < NDIM; d++) {
+            const double x = (fabs(ww[1 + d]) + c) * g.rdx[lev][d];
+            m = x > m ? x : m;
+        }
+        mn = fmin(mn, rcp(m));
+    }
+    if (!ok) flag_nonphysical(sc);
+    block_min_to(mn, red, &sc->acc);
+}
+
+unsigned grid_of(long long n) {
+    long long b = (n + 255) / 256;
+    return (unsigned)std::max(1LL, std::min(b, 148LL * 16));
+}
+
+}  // namespace
+}  // namespace spark
+
+// ===================================================================== host
+namespace {
+
+using spark::AmrGeo;
+using spark::CorrE;
+using spark::GuardE;
+
+struct AmrError : std::runtime_error {
+    spark_status st;
+    AmrError(spark_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+#define ACU(call)                                                                                      \
+    do {                                                                                               \
+        cudaError_t e_ = (call);                                                                       \
+        if (e_ != cudaSuccess) throw AmrError(SPARK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+int recon_ng(int recon) { return (recon == 2 || recon == 4) ? 3 : ((recon == 1 || recon == 3) ? 2 : 1); }
+
+bool has_box(const spark_refine* r) {
+    for (int d = 0; d < 3; d++)
+        if (r->rhi[d] <= r->rlo[d]) return false;
+    return true;
+}
+
+// Host plan of the composite grid: leaves, guard map, correction lists.
+struct AmrPlan {
+    spark_config c{};
+    spark_refine r{};
+    AmrGeo g{};
+    std::vector<int> level;
+    std::vector<std::array<long long, 3>> blk;
+    std::vector<GuardE> guards;
+    std::vector<CorrE> corr[3];
+    long long fnb[3] = {1, 1, 1};
+
+    bool refined(const long long* cb) const {
+        if (!has_box(&r)) return false;
+        for (int d = 0; d < 3; d++)
+            if (cb[d] < r.rlo[d] || cb[d] >= r.rhi[d]) return false;
+        return true;
+    }
+    long long ncells(int lev, int d) const {
+        const long long n = (long long)c.nblk[d] * c.nb[d];
+        return d < c.ndim ? n << lev : n;
+    }
+    // level-L block coordinates -> leaf (-1 if none)
+    long long leaf_of(int lev, const long long* b) const {
+        if (lev == 1) {
+            long long q[3];
+            for (int d = 0; d < 3; d++) {
+                q[d] = b[d] - (d < c.ndim ? 2LL * r.rlo[d] : 0);
+                if (q[d] < 0 || q[d] >= fnb[d]) return -1;
+            }
+            return g.ncl + q[0] + fnb[0] * (q[1] + fnb[1] * q[2]);
+        }
+        if (refined(b)) return -1;
+        return coarse_index[(b[2] * c.nblk[1] + b[1]) * c.nblk[0] + b[0]];
+    }
+    std::vector<long long> coarse_index;
+};
+
+std::string check_amr(const spark_config* c, const spark_refine* r) {
+    if (!c || !r) return "null argument";
+    if (c->ndim < 1 || c->ndim > 3) return "ndim must be 1..3";
+    if (c->recon < 0 || c->recon > 4 || c->riemann < 0 || c->riemann > 2) return "unknown recon / riemann";
+    if (c->rk_stages != 2 && c->rk_stages != 3) return "rk_stages must be 2 or 3";
+    if (!(c->gamma > 1.0) || !(c->cfl > 0.0)) return "gamma must be > 1 and cfl > 0";
+    if (c->ng < recon_ng(c->recon)) return "ng too small for the reconstruction";
+    if (c->riemann == 2 && (recon_ng(c->recon) < 2 || !(c->shock_thresh > 0.0)))
+        return "hybrid Riemann needs recon >= PLM and shock_thresh > 0";
+    for (int d = 0; d < 3; d++) {
+        if (c->grav[d] != 0.0) return "gravity is not supported on the refined grid";
+        if (c->nb[d] < 1 || c->nblk[d] < 1) return "nb and nblk must be >= 1";
+        if (d >= c->ndim && (c->nb[d] != 1 || c->nblk[d] != 1)) return "unused dims need nb = nblk = 1";
+        if (d < c->ndim && c->nb[d] < c->ng) return "nb must be >= ng";
+        if (d < c->ndim && !(c->hi[d] > c->lo[d])) return "hi must exceed lo";
+        for (int s = 0; s < 2; s++)
+            if (c->bc[d][s] < 0 || c->bc[d][s] > 2) return "unknown boundary condition";
+        if (d < c->ndim && (c->bc[d][0] == SPARK_BC_PERIODIC) != (c->bc[d][1] == SPARK_BC_PERIODIC))
+            return "periodic boundaries must be periodic on both sides";
+        if (r->rlo[d] < 0 || r->rhi[d] > c->nblk[d] || r->rlo[d] > r->rhi[d]) return "refined box outside the grid";
+    }
+    if (has_box(r))
+        for (int d = 0; d < 3; d++) {
+            if (d < c->ndim && c->nb[d] % 2) return "nb must be even with a refined box";
+            if (d >= c->ndim && (r->rlo[d] != 0 || r->rhi[d] != 1)) return "unused dims of the box must be [0, 1)";
+        }
+    const long long plane = (long long)c->nb[0] * c->nb[1] * c->nb[2];
+    if (plane * (long long)c->nblk[0] * c->nblk[1] * c->nblk[2] * 8 > (1LL << 33)) return "grid too large";
+    return "";
+}
+
+// Per-dimension boundary map at one level (periodic wrap / outflow clamp /
+// reflect mirror); *flip set for a reflect.
+long long bmap(long long g, long long N, int lo, int hi, bool* flip) {
+    *flip = false;
+    if (g >= 0 && g < N) return g;
+    const int bc = g < 0 ? lo : hi;
+    if (bc == SPARK_BC_PERIODIC) return ((g % N) + N) % N;
+    if (bc == SPARK_BC_OUTFLOW) return g < 0 ? 0 : N - 1;
+    *flip = true;
+    return g < 0 ? -1 - g : 2 * N - 1 - g;
+}
+
+AmrPlan make_amr_plan(const spark_config* c, const spark_refine* r) {
+    std::string m = check_amr(c, r);
+    if (!m.empty()) throw AmrError(SPARK_ERR_ARG, m);
+    AmrPlan p;
+    p.c = *c;
+    p.r = *r;
+    const int nd = c->ndim;
+    AmrGeo& g = p.g;
+    g.ndim = nd;
+    g.nv = nd + 2;
+    g.ng = c->ng;
+    g.ngk = recon_ng(c->recon);
+    g.recon = c->recon;
+    g.np = 1;
+    g.nc = 1;
+    for (int d = 0; d < 3; d++) {
+        g.nb[d] = c->nb[d];
+        g.pn[d] = c->nb[d] + (d < nd ? 2 * c->ng : 0);
+        g.np *= g.pn[d];
+        g.nc *= c->nb[d];
+        const double dx = (c->hi[d] - c->lo[d]) / ((double)c->nblk[d] * c->nb[d]);
+        g.rdx[0][d] = 1.0 / dx;
+        g.rdx[1][d] = 1.0 / (0.5 * dx);
+        p.fnb[d] = has_box(r) ? (d < nd ? 2LL * (r->rhi[d] - r->rlo[d]) : 1) : 0;
+    }
+    // leaves
+    p.coarse_index.assign((size_t)c->nblk[0] * c->nblk[1] * c->nblk[2], -1);
+    for (long long bz = 0; bz < c->nblk[2]; bz++)
+        for (long long by = 0; by < c->nblk[1]; by++)
+            for (long long bx = 0; bx < c->nblk[0]; bx++) {
+                const long long b[3] = {bx, by, bz};
+                if (p.refined(b)) continue;
+                p.coarse_index[(bz * c->nblk[1] + by) * c->nblk[0] + bx] = (long long)p.level.size();
+                p.level.push_back(0);
+                p.blk.push_back({bx, by, bz});
+            }
+    g.ncl = (long long)p.level.size();
+    if (has_box(r))
+        for (long long bz = 0; bz < p.fnb[2]; bz++)
+            for (long long by = 0; by < p.fnb[1]; by++)
+                for (long long bx = 0; bx < p.fnb[0]; bx++) {
+                    p.level.push_back(1);
+                    p.blk.push_back({2LL * r->rlo[0] + bx, nd >= 2 ? 2LL * r->rlo[1] + by : 0,
+                                     nd >= 3 ? 2LL * r->rlo[2] + bz : 0});
+                }
+    g.nleaf = (long long)p.level.size();
+    // faces
+    long long off = 0;
+    g.mf = 1;
+    for (int d = 0; d < 3; d++) {
+        g.Fo[d] = off;
+        g.nfd[d] = 0;
+        if (d < nd) {
+            g.nfd[d] = 1;
+            for (int e = 0; e < 3; e++) g.nfd[d] *= c->nb[e] + (e == d ? 1 : 0);
+            long long fcells = 1;
+            for (int e = 0; e < nd; e++)
+                if (e != d) fcells *= c->nb[e];
+            g.mf = std::max(g.mf, fcells);
+        }
+        off += g.nfd[d];
+    }
+    g.NF = off;
+    g.gamma = c->gamma;
+    g.cfl = c->cfl;
+    g.shock_thresh = c->riemann == 2 ? c->shock_thresh : 0.0;
+    // guard map: every face guard of every leaf (reading R22)
+    for (long long leaf = 0; leaf < g.nleaf; leaf++) {
+        const int lev = p.level[leaf];
+        const auto& b = p.blk[leaf];
+        for (int d = 0; d < nd; d++) {
+            int tr[2] = {-1, -1}, nt = 0;  // the transverse dimensions of d, increasing
+            for (int e = 0; e < nd; e++)
+                if (e != d) tr[nt++] = e;
+            for (int side = 0; side < 2; side++)
+                for (int depth = 0; depth < c->ng; depth++)
+                    for (int t2 = 0; t2 < (nt > 1 ? c->nb[tr[1]] : 1); t2++)
+                        for (int t1 = 0; t1 < (nt > 0 ? c->nb[tr[0]] : 1); t1++) {
+                            int loc[3] = {0, 0, 0};
+                            loc[d] = side ? c->nb[d] + depth : -1 - depth;
+                            if (nt > 0) loc[tr[0]] = t1;
+                            if (nt > 1) loc[tr[1]] = t2;
+                            long long gc[3];
+                            for (int e = 0; e < 3; e++) gc[e] = b[e] * c->nb[e] + loc[e];
+                            bool flip;
+                            gc[d] = bmap(gc[d], p.ncells(lev, d), c->bc[d][0], c->bc[d][1], &flip);
+                            GuardE E{};
+                            int gpad[3];
+                            for (int e = 0; e < 3; e++) gpad[e] = e < nd ? c->ng : 0;
+                            E.dst = leaf * g.np +
+                                    ((long long)(loc[2] + gpad[2]) * g.pn[1] + (loc[1] + gpad[1])) * g.pn[0] + (loc[0] + gpad[0]);
+                            E.kind = flip ? (1 << (4 + d)) : 0;
+                            auto cell_of = [&](int lv, const long long* x, long long* leaf_out) {
+                                long long bb[3], cc[3];
+                                for (int e = 0; e < 3; e++) bb[e] = x[e] / c->nb[e], cc[e] = x[e] % c->nb[e];
+                                *leaf_out = p.leaf_of(lv, bb);
+                                return (cc[2] * c->nb[1] + cc[1]) * c->nb[0] + cc[0];
+                            };
+                            long long src_leaf;
+                            if (lev == 1) {
+                                long long cg[3], cb[3];
+                                for (int e = 0; e < 3; e++) {
+                                    cg[e] = e < nd ? gc[e] / 2 : gc[e];
+                                    cb[e] = cg[e] / c->nb[e];
+                                }
+                                if (p.refined(cb)) {
+                                    const long long cell = cell_of(1, gc, &src_leaf);
+                                    E.src = src_leaf * g.nc + cell;
+                                } else {  // prolongation: the containing coarse cell (injection)
+                                    const long long cell = cell_of(0, cg, &src_leaf);
+                                    E.src = src_leaf * g.nc + cell;
+                                }
+                                E.kind |= 1;
+                            } else {
+                                long long cb[3];
+                                for (int e = 0; e < 3; e++) cb[e] = gc[e] / c->nb[e];
+                                if (!p.refined(cb)) {
+                                    const long long cell = cell_of(0, gc, &src_leaf);
+                                    E.src = src_leaf * g.nc + cell;
+                                    E.kind |= 1;
+                                } else {  // restriction: the 2^ndim fine children, first child here
+                                    long long fg[3];
+                                    for (int e = 0; e < 3; e++) fg[e] = e < nd ? 2 * gc[e] : gc[e];
+                                    const long long cell = cell_of(1, fg, &src_leaf);
+                                    E.src = src_leaf * g.nc + cell;
+                                    E.kind |= 2;
+                                }
+                            }
+                            if (src_leaf < 0) throw AmrError(SPARK_ERR_ARG, "internal: guard source is not a leaf");
+                            p.guards.push_back(E);
+                        }
+        }
+    }
+    // correction lists (communicate_fluxes): coarse faces on a coarse-fine interface
+    if (has_box(r))
+        for (long long leaf = 0; leaf < g.ncl; leaf++) {
+            const auto& b = p.blk[leaf];
+            for (int d = 0; d < nd; d++)
+                for (int side = 0; side < 2; side++) {
+                    const long long N0 = p.ncells(0, d);
+                    const long long gface = side ? (b[d] + 1) * c->nb[d] : b[d] * c->nb[d] - 1;
+                    if ((gface < 0 || gface >= N0) && c->bc[d][side] != SPARK_BC_PERIODIC) continue;
+                    bool fl;
+                    const long long gm = bmap(gface, N0, c->bc[d][0], c->bc[d][1], &fl);
+                    long long nbk[3] = {b[0], b[1], b[2]};
+                    nbk[d] = gm / c->nb[d];
+                    if (!p.refined(nbk)) continue;
+                    const long long fd = side ? 2 * gm : 2 * gm + 1;
+                    const int e1 = d == 0 ? 1 : 0, e2 = d == 2 ? 1 : 2;
+                    const int n1 = nd > 1 ? c->nb[e1] : 1, n2 = nd > 2 ? c->nb[e2] : 1;
+                    for (int t2 = 0; t2 < n2; t2++)
+                        for (int t1 = 0; t1 < n1; t1++) {
+                            int lc[3] = {0, 0, 0};
+                            lc[d] = side ? c->nb[d] - 1 : 0;
+                            if (nd > 1) lc[e1] = t1;
+                            if (nd > 2) lc[e2] = t2;
+                            CorrE E{};
+                            E.cell = leaf * g.nc + ((long long)lc[2] * c->nb[1] + lc[1]) * c->nb[0] + lc[0];
+                            E.bc = (leaf * 6 + 2 * d + side) * g.mf + spark::face_cell(g, d, lc[0], lc[1], lc[2]);
+                            E.side = side;
+                            const int nf = 1 << (nd - 1);
+                            for (int q = 0; q < nf; q++) {
+                                long long fg[3] = {0, 0, 0};
+                                fg[d] = fd;
+                                if (nd > 1) fg[e1] = 2 * (b[e1] * c->nb[e1] + t1) + (q & 1);
+                                if (nd > 2) fg[e2] = 2 * (b[e2] * c->nb[e2] + t2) + ((q >> 1) & 1);
+                                long long fb[3], flc[3];
+                                for (int e = 0; e < 3; e++) fb[e] = fg[e] / c->nb[e], flc[e] = fg[e] % c->nb[e];
+                                const long long fleaf = p.leaf_of(1, fb);
+                                if (fleaf < 0) throw AmrError(SPARK_ERR_ARG, "internal: fine face is not a leaf");
+                                E.bf[q] = (fleaf * 6 + 2 * d + (1 - side)) * g.mf +
+                                          spark::face_cell(g, d, (int)flc[0], (int)flc[1], (int)flc[2]);
+                            }
+                            p.corr[d].push_back(E);
+                        }
+                }
+        }
+    return p;
+}
+
+size_t al(size_t x) { return (x + 255) / 256 * 256; }
+
+size_t amr_bytes(const AmrPlan& p) {
+    const AmrGeo& g = p.g;
+    size_t b = al(sizeof(spark::DevScalars));
+    b += 3 * al(sizeof(double) * g.nv * g.nleaf * g.nc);       // U^n and two stage buffers
+    b += al(sizeof(double) * g.nv * g.nleaf * g.np);            // padded tiles
+    b += al(sizeof(double) * g.nv * g.nleaf * g.NF);            // face fluxes
+    b += al(sizeof(double) * g.nv * g.nleaf * 6 * g.mf);        // fluxBuff
+    b += al(sizeof(GuardE) * std::max<size_t>(1, p.guards.size()));
+    for (int d = 0; d < 3; d++) b += al(sizeof(CorrE) * std::max<size_t>(1, p.corr[d].size()));
+    return b;
+}
+
+}  // namespace
+
+struct spark_amr {
+    AmrPlan plan;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    spark::DevScalars* sc = nullptr;
+    double* U[3] = {};
+    double* W = nullptr;
+    double* F = nullptr;
+    double* B = nullptr;
+    GuardE* guards = nullptr;
+    CorrE* corr[3] = {};
+    int n_idx = 0;
+    bool have_state = false;
+    std::string err;
+};
+
+namespace {
+
+template <typename Fn>
+spark_status amr_guard(spark_amr* a, Fn&& f) {
+    try {
+        if (a) a->err.clear();
+        f();
+        return SPARK_OK;
+    } catch (const AmrError& e) {
+        if (a) a->err = e.what();
+        return e.st;
+    } catch (const std::exception& e) {
+        if (a) a->err = e.what();
+        return SPARK_ERR_ARG;
+    }
+}
+
+void launched(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw AmrError(SPARK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// padded tiles of state u: interior + face guards; primitives (to_prim) or conserved
+void amr_fill(spark_amr* a, const double* u, double* w, int to_prim) {
+    const AmrGeo& g = a->plan.g;
+    const long long nG = (long long)a->plan.guards.size();
+    const unsigned gi = spark::grid_of(g.nleaf * g.nc), gg = spark::grid_of(nG);
+    if (g.ndim == 1) {
+        spark::amr_interior_kernel<3><<<gi, 256, 0, a->stream>>>(g, u, w, to_prim, a->sc);
+        if (nG) spark::amr_guard_kernel<3><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, w, to_prim, a->sc);
+    } else if (g.ndim == 2) {
+        spark::amr_interior_kernel<4><<<gi, 256, 0, a->stream>>>(g, u, w, to_prim, a->sc);
+        if (nG) spark::amr_guard_kernel<4><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, w, to_prim, a->sc);
+    } else {
+        spark::amr_interior_kernel<5><<<gi, 256, 0, a->stream>>>(g, u, w, to_prim, a->sc);
+        if (nG) spark::amr_guard_kernel<5><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, w, to_prim, a->sc);
+    }
+    launched(cudaGetLastError(), "amr fill");
+}
+
+template <int NDIM>
+void faces_d(spark_amr* a, double bco) {
+    const AmrGeo& g = a->plan.g;
+    const unsigned gr = spark::grid_of(g.nleaf * g.NF);
+    const int rs = a->plan.c.riemann;
+    if (rs == 0) spark::amr_face_kernel<NDIM, 0><<<gr, 256, 0, a->stream>>>(g, a->W, a->F, a->B, bco);
+    else if (rs == 1) spark::amr_face_kernel<NDIM, 1><<<gr, 256, 0, a->stream>>>(g, a->W, a->F, a->B, bco);
+    else spark::amr_face_kernel<NDIM, 2><<<gr, 256, 0, a->stream>>>(g, a->W, a->F, a->B, bco);
+    launched(cudaGetLastError(), "amr faces");
+}
+
+void amr_stage(spark_amr* a, const double* prev, const double* un, double sa, double sb, double* out) {
+    const AmrGeo& g = a->plan.g;
+    amr_fill(a, prev, a->W, 1);
+    if (g.ndim == 1) faces_d<1>(a, sb);
+    else if (g.ndim == 2) faces_d<2>(a, sb);
+    else faces_d<3>(a, sb);
+    const unsigned gr = spark::grid_of(g.nleaf * g.nc);
+    if (g.ndim == 1) spark::amr_update_kernel<1><<<gr, 256, 0, a->stream>>>(g, a->F, prev, un, out, sa, sb, a->sc);
+    else if (g.ndim == 2) spark::amr_update_kernel<2><<<gr, 256, 0, a->stream>>>(g, a->F, prev, un, out, sa, sb, a->sc);
+    else spark::amr_update_kernel<3><<<gr, 256, 0, a->stream>>>(g, a->F, prev, un, out, sa, sb, a->sc);
+    launched(cudaGetLastError(), "amr update");
+}
+
+void amr_cfl(spark_amr* a, const double* u) {
+    const AmrGeo& g = a->plan.g;
+    const unsigned gr = spark::grid_of(g.nleaf * g.nc);
+    if (g.ndim == 1) spark::amr_cfl_kernel<1><<<gr, 256, 0, a->stream>>>(g, u, a->sc);
+    else if (g.ndim == 2) spark::amr_cfl_kernel<2><<<gr, 256, 0, a->stream>>>(g, u, a->sc);
+    else spark::amr_cfl_kernel<3><<<gr, 256, 0, a->stream>>>(g, u, a->sc);
+    launched(cudaGetLastError(), "amr cfl");
+}
+
+void amr_correct(spark_amr* a, double* u) {
+    const AmrGeo& g = a->plan.g;
+    for (int d = 0; d < g.ndim; d++) {  // one launch per direction: no two threads touch one cell
+        const long long n = (long long)a->plan.corr[d].size();
+        if (!n) continue;
+        const unsigned gr = spark::grid_of(n);
+        if (g.ndim == 1) spark::amr_corr_kernel<3><<<gr, 256, 0, a->stream>>>(g, a->corr[d], n, d, a->B, u, &a->sc->dt, a->sc);
+        else if (g.ndim == 2) spark::amr_corr_kernel<4><<<gr, 256, 0, a->stream>>>(g, a->corr[d], n, d, a->B, u, &a->sc->dt, a->sc);
+        else spark::amr_corr_kernel<5><<<gr, 256, 0, a->stream>>>(g, a->corr[d], n, d, a->B, u, &a->sc->dt, a->sc);
+        launched(cudaGetLastError(), "amr correction");
+    }
+}
+
+spark::DevScalars read_sc(spark_amr* a) {
+    ACU(cudaStreamSynchronize(a->stream));
+    spark::DevScalars h;
+    ACU(cudaMemcpy(&h, a->sc, sizeof(h), cudaMemcpyDeviceToHost));
+    return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+spark_status spark_amr_leaves(const spark_config* cfg, const spark_refine* ref, int64_t* ncoarse, int64_t* nfine) {
+    return amr_guard(nullptr, [&] {
+        AmrPlan p = make_amr_plan(cfg, ref);
+        if (ncoarse) *ncoarse = p.g.ncl;
+        if (nfine) *nfine = p.g.nleaf - p.g.ncl;
+    });
+}
+
+spark_status spark_amr_required_bytes(const spark_config* cfg, const spark_refine* ref, size_t* bytes) {
+    return amr_guard(nullptr, [&] {
+        if (!bytes) throw AmrError(SPARK_ERR_ARG, "null bytes");
+        *bytes = amr_bytes(make_amr_plan(cfg, ref));
+    });
+}
+
+spark_status spark_amr_init(const spark_config* cfg, const spark_refine* ref, int32_t device, void* cuda_stream,
+                            void* arena, size_t arena_bytes, spark_amr** out) {
+    if (!out) return SPARK_ERR_ARG;
+    *out = nullptr;
+    std::unique_ptr<spark_amr> a(new spark_amr());
+    spark_status st = amr_guard(nullptr, [&] {
+        a->plan = make_amr_plan(cfg, ref);
+        a->device = device;
+        a->stream = static_cast<cudaStream_t>(cuda_stream);
+        const size_t need = amr_bytes(a->plan);
+        if (!arena) throw AmrError(SPARK_ERR_ARG, "null arena");
+        if (arena_bytes < need) throw AmrError(SPARK_ERR_OOM, "arena smaller than spark_amr_required_bytes");
+        if (reinterpret_cast<uintptr_t>(arena) % 256) throw AmrError(SPARK_ERR_ARG, "arena must be 256-byte aligned");
+        ACU(cudaSetDevice(device));
+        const AmrGeo& g = a->plan.g;
+        char* p = static_cast<char*>(arena);
+        a->sc = reinterpret_cast<spark::DevScalars*>(p);
+        p += al(sizeof(spark::DevScalars));
+        for (int i = 0; i < 3; i++) {
+            a->U[i] = reinterpret_cast<double*>(p);
+            p += al(sizeof(double) * g.nv * g.nleaf * g.nc);
+        }
+        a->W = reinterpret_cast<double*>(p);
+        p += al(sizeof(double) * g.nv * g.nleaf * g.np);
+        a->F = reinterpret_cast<double*>(p);
+        p += al(sizeof(double) * g.nv * g.nleaf * g.NF);
+        a->B = reinterpret_cast<double*>(p);
+        p += al(sizeof(double) * g.nv * g.nleaf * 6 * g.mf);
+        a->guards = reinterpret_cast<GuardE*>(p);
+        p += al(sizeof(GuardE) * std::max<size_t>(1, a->plan.guards.size()));
+        if (!a->plan.guards.empty())
+            ACU(cudaMemcpyAsync(a->guards, a->plan.guards.data(), sizeof(GuardE) * a->plan.guards.size(),
+                                cudaMemcpyHostToDevice, a->stream));
+        for (int d = 0; d < 3; d++) {
+            a->corr[d] = reinterpret_cast<CorrE*>(p);
+            p += al(sizeof(CorrE) * std::max<size_t>(1, a->plan.corr[d].size()));
+            if (!a->plan.corr[d].empty())
+                ACU(cudaMemcpyAsync(a->corr[d], a->plan.corr[d].data(), sizeof(CorrE) * a->plan.corr[d].size(),
+                                    cudaMemcpyHostToDevice, a->stream));
+        }
+        launched(spark::launch_scalars_reset(a->sc, a->stream), "scalars reset");
+        ACU(cudaStreamSynchronize(a->stream));  // the host plan vectors are the copy sources
+    });
+    if (st == SPARK_OK) *out = a.release();
+    return st;
+}
+
+spark_status spark_amr_finalize(spark_amr* a) {
+    if (!a) return SPARK_ERR_ARG;
+    spark_status st = amr_guard(a, [&] { ACU(cudaStreamSynchronize(a->stream)); });
+    delete a;
+    return st;
+}
+
+const char* spark_amr_last_error(const spark_amr* a) { return a ? a->err.c_str() : "null context"; }
+
+spark_status spark_amr_set_state(spark_amr* a, const double* U, int32_t on_device) {
+    if (!a || !U) return SPARK_ERR_ARG;
+    return amr_guard(a, [&] {
+        ACU(cudaSetDevice(a->device));
+        const AmrGeo& g = a->plan.g;
+        a->n_idx = 0;
+        ACU(cudaMemcpyAsync(a->U[0], U, sizeof(double) * g.nv * g.nleaf * g.nc,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, a->stream));
+        launched(spark::launch_scalars_reset(a->sc, a->stream), "scalars reset");
+        amr_cfl(a, a->U[0]);
+        a->have_state = true;
+    });
+}
+
+spark_status spark_amr_get_state(spark_amr* a, double* U, int32_t on_device) {
+    if (!a || !U) return SPARK_ERR_ARG;
+    return amr_guard(a, [&] {
+        if (!a->have_state) throw AmrError(SPARK_ERR_STATE, "no state loaded");
+        ACU(cudaSetDevice(a->device));
+        const AmrGeo& g = a->plan.g;
+        ACU(cudaMemcpyAsync(U, a->U[a->n_idx], sizeof(double) * g.nv * g.nleaf * g.nc,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, a->stream));
+        spark::DevScalars h = read_sc(a);
+        if (h.bad != spark::kNoBad)
+            throw AmrError(SPARK_ERR_NONPHYSICAL, "non-physical state in step " + std::to_string(h.bad));
+    });
+}
+
+spark_status spark_amr_fill_guardcells(spark_amr* a, double* padded_out) {
+    if (!a || !padded_out) return SPARK_ERR_ARG;
+    return amr_guard(a, [&] {
+        if (!a->have_state) throw AmrError(SPARK_ERR_STATE, "no state loaded");
+        ACU(cudaSetDevice(a->device));
+        const AmrGeo& g = a->plan.g;
+        // corners / edges are never written: NaN, as in the oracle
+        ACU(cudaMemsetAsync(padded_out, 0xff, sizeof(double) * g.nv * g.nleaf * g.np, a->stream));
+        amr_fill(a, a->U[a->n_idx], padded_out, 0);
+    });
+}
+
+spark_status spark_amr_step(spark_amr* a, double dt, double t_end, double* dt_used) {
+    if (!a) return SPARK_ERR_ARG;
+    return amr_guard(a, [&] {
+        if (!a->have_state) throw AmrError(SPARK_ERR_STATE, "no state loaded");
+        ACU(cudaSetDevice(a->device));
+        const AmrGeo& g = a->plan.g;
+        const int S = a->plan.c.rk_stages, n = a->n_idx;
+        const int x = (n + 1) % 3, y = (n + 2) % 3;
+        launched(spark::launch_step_begin(a->sc, dt, t_end, a->plan.c.cfl, a->stream), "step begin");
+        ACU(cudaMemsetAsync(a->B, 0, sizeof(double) * g.nv * g.nleaf * 6 * g.mf, a->stream));
+        // Shu-Osher stages: RK2 n->x, (x,n)->y; RK3 n->x, (x,n)->y, (y,n)->x
+        static const double ca[3][3] = {{0.0, 0.5, 0.0}, {0.0, 0.75, 1.0 / 3.0}, {0, 0, 0}};
+        static const double cb[3][3] = {{1.0, 0.5, 0.0}, {1.0, 0.25, 2.0 / 3.0}, {0, 0, 0}};
+        const int row = S == 2 ? 0 : 1;
+        const int prev[3] = {n, x, y}, outb[3] = {x, y, x};
+        for (int s = 0; s < S; s++)
+            amr_stage(a, a->U[prev[s]], a->U[n], ca[row][s], cb[row][s], a->U[outb[s]]);
+        const int newn = S == 2 ? y : x;
+        amr_correct(a, a->U[newn]);  // communicate_fluxes + flux correction
+        amr_cfl(a, a->U[newn]);      // CFL minimum of the corrected state: dt of the next step
+        a->n_idx = newn;
+        if (dt_used) {
+            spark::DevScalars h = read_sc(a);
+            if (h.bad != spark::kNoBad) {
+                if (h.active && h.bad == (unsigned long long)h.steps) {  // roll back this step
+                    a->n_idx = n;
+                    h.t = h.t_prev;
+                    h.steps -= 1;
+                    h.acc = h.acc_prev;
+                    h.bad = spark::kNoBad;
+                    h.status = 0;
+                    ACU(cudaMemcpy(a->sc, &h, sizeof(h), cudaMemcpyHostToDevice));
+                    throw AmrError(SPARK_ERR_NONPHYSICAL, "non-physical state; rolled back to U^n");
+                }
+                throw AmrError(SPARK_ERR_NONPHYSICAL, "non-physical state in step " + std::to_string(h.bad) +
+                                                          "; later steps were frozen, state not rolled back");
+            }
+            *dt_used = h.dt;
+        }
+    });
+}
+
+spark_status spark_amr_get_time(spark_amr* a, double* t, int64_t* steps, double* dt_last) {
+    if (!a) return SPARK_ERR_ARG;
+    return amr_guard(a, [&] {
+        spark::DevScalars h = read_sc(a);
+        if (t) *t = h.t;
+        if (steps) *steps = h.steps;
+        if (dt_last) *dt_last = h.dt;
+    });
+}
+
+}  // extern "C"

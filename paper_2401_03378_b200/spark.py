@@ -26,6 +26,8 @@ EXPORTS = [
     "spark_get_time", "spark_get_cfl_min", "spark_fill_guardcells", "spark_step", "spark_advance",
     "spark_step_group", "spark_stage_apply", "spark_profile_enable", "spark_profile_read",
     "spark_selftest_riemann", "spark_axpy", "spark_step_telescoping", "spark_run", "spark_set_time",
+    "spark_amr_leaves", "spark_amr_required_bytes", "spark_amr_init", "spark_amr_finalize", "spark_amr_last_error",
+    "spark_amr_set_state", "spark_amr_get_state", "spark_amr_fill_guardcells", "spark_amr_step", "spark_amr_get_time",
 ]
 
 
@@ -56,6 +58,10 @@ class CConfig(ctypes.Structure):
         ("grav", ctypes.c_double * 3),
         ("shock_thresh", ctypes.c_double),
     ]
+
+
+class CRefine(ctypes.Structure):
+    _fields_ = [("rlo", ctypes.c_int32 * 3), ("rhi", ctypes.c_int32 * 3)]
 
 
 class CFacePlan(ctypes.Structure):
@@ -118,6 +124,16 @@ def lib() -> ctypes.CDLL:
         "spark_get_time": (i32, [vp, P(d), P(i64), P(d)]),
         "spark_get_cfl_min": (i32, [vp, P(d)]),
         "spark_set_time": (i32, [vp, d, i64]),
+        "spark_amr_leaves": (i32, [cp, P(CRefine), P(i64), P(i64)]),
+        "spark_amr_required_bytes": (i32, [cp, P(CRefine), P(ctypes.c_size_t)]),
+        "spark_amr_init": (i32, [cp, P(CRefine), i32, vp, vp, ctypes.c_size_t, P(vp)]),
+        "spark_amr_finalize": (i32, [vp]),
+        "spark_amr_last_error": (ctypes.c_char_p, [vp]),
+        "spark_amr_set_state": (i32, [vp, vp, i32]),
+        "spark_amr_get_state": (i32, [vp, vp, i32]),
+        "spark_amr_fill_guardcells": (i32, [vp, vp]),
+        "spark_amr_step": (i32, [vp, d, d, P(d)]),
+        "spark_amr_get_time": (i32, [vp, P(d), P(i64), P(d)]),
         "spark_fill_guardcells": (i32, [vp, vp]),
         "spark_step": (i32, [vp, d, d, P(d)]),
         "spark_advance": (i32, [vp, i64, d, i32, P(i64)]),
@@ -401,3 +417,103 @@ class LocalGroup:
     def close(self):
         for r in self.ranks:
             r.close()
+
+
+# ------------------------------------------------ NEXT N3: static two-level AMR
+def _refine(rlo, rhi) -> CRefine:
+    r = CRefine()
+    for d in range(3):
+        r.rlo[d] = int(rlo[d])
+        r.rhi[d] = int(rhi[d])
+    return r
+
+
+def amr_leaves(cfg: dict, rlo, rhi):
+    c, r = to_cconfig(cfg), _refine(rlo, rhi)
+    nc, nf = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().spark_amr_leaves(ctypes.byref(c), ctypes.byref(r), ctypes.byref(nc), ctypes.byref(nf)),
+           what="amr_leaves")
+    return nc.value, nf.value
+
+
+class Amr:
+    """A static two-level refinement (spark_amr_*): coarse blocks [rlo, rhi)
+    refined by 2; state U[v][leaf][k][j][i] (coarse leaves, then fine)."""
+
+    def __init__(self, cfg: dict, rlo, rhi, device: Optional[int] = None, stream=None):
+        import torch
+
+        self.torch = torch
+        self.cfg = dict(cfg)
+        self.device = torch.cuda.current_device() if device is None else device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        nc, nf = amr_leaves(cfg, rlo, rhi)
+        self.nleaf = nc + nf
+        self.shape = (cfg["ndim"] + 2, self.nleaf) + tuple(reversed(cfg["nb"]))
+        c, r = to_cconfig(cfg), _refine(rlo, rhi)
+        nbytes = ctypes.c_size_t()
+        _check(lib().spark_amr_required_bytes(ctypes.byref(c), ctypes.byref(r), ctypes.byref(nbytes)),
+               what="amr_required_bytes")
+        self.arena = torch.empty(nbytes.value, dtype=torch.uint8, device=f"cuda:{self.device}")
+        h = ctypes.c_void_p()
+        st = lib().spark_amr_init(ctypes.byref(c), ctypes.byref(r), self.device,
+                                  ctypes.c_void_p(self.stream.cuda_stream), ctypes.c_void_p(self.arena.data_ptr()),
+                                  nbytes.value, ctypes.byref(h))
+        _check(st, what="amr_init")
+        self.ctx = h
+
+    def _chk(self, st, what):
+        if st != SPARK_OK:
+            msg = lib().spark_amr_last_error(self.ctx).decode()
+            text = f"{what}: {lib().spark_status_string(st).decode()} — {msg}"
+            raise (NonPhysicalError if st == SPARK_ERR_NONPHYSICAL else SparkError)(st, text)
+
+    def set_state(self, U):
+        torch = self.torch
+        if isinstance(U, torch.Tensor):
+            if not (U.is_cuda and U.dtype == torch.float64 and U.is_contiguous() and tuple(U.shape) == self.shape):
+                raise ValueError("U must be a contiguous float64 CUDA tensor of the leaf shape")
+            self._chk(lib().spark_amr_set_state(self.ctx, ctypes.c_void_p(U.data_ptr()), 1), "amr_set_state")
+        else:
+            U = np.ascontiguousarray(U, dtype=np.float64)
+            if U.shape != self.shape:
+                raise ValueError(f"U has shape {U.shape}, expected {self.shape}")
+            self._chk(lib().spark_amr_set_state(self.ctx, ctypes.c_void_p(U.ctypes.data), 0), "amr_set_state")
+            self.stream.synchronize()
+
+    def get_state(self):
+        out = np.empty(self.shape, dtype=np.float64)
+        self._chk(lib().spark_amr_get_state(self.ctx, ctypes.c_void_p(out.ctypes.data), 0), "amr_get_state")
+        return out
+
+    def fill_guardcells(self):
+        ng = self.cfg["ng"]
+        nd = self.cfg["ndim"]
+        pn = [self.cfg["nb"][d] + (2 * ng if d < nd else 0) for d in range(3)]
+        out = self.torch.empty((nd + 2, self.nleaf, pn[2], pn[1], pn[0]), dtype=self.torch.float64,
+                               device=f"cuda:{self.device}")
+        self._chk(lib().spark_amr_fill_guardcells(self.ctx, ctypes.c_void_p(out.data_ptr())), "amr_fill")
+        self.stream.synchronize()
+        return out
+
+    def step(self, dt: float = 0.0, t_end: float = 0.0, sync: bool = False):
+        d = ctypes.c_double()
+        self._chk(lib().spark_amr_step(self.ctx, dt, t_end, ctypes.byref(d) if sync else None), "amr_step")
+        return d.value if sync else None
+
+    def time(self):
+        t, dt = ctypes.c_double(), ctypes.c_double()
+        n = ctypes.c_int64()
+        self._chk(lib().spark_amr_get_time(self.ctx, ctypes.byref(t), ctypes.byref(n), ctypes.byref(dt)), "amr_time")
+        return t.value, n.value, dt.value
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib().spark_amr_finalize(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -148,3 +148,31 @@ def test_product_path_does_not_touch_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "spark_oracle" not in txt and "libspark_oracle" not in txt, f
+
+
+def test_amr_host_plan_matches_oracle_leaf_count():
+    """NEXT N3 host logic (no GPU): the leaf enumeration of spark_amr_leaves
+    agrees with the oracle's and with spark_inputs' layout helper; invalid
+    refinements are refused; the arena size grows with the fine leaves."""
+    from paper_2401_03378_b200 import spark
+
+    import oracle
+    import spark_inputs as si
+
+    p = si.Problem("a", 3, (8, 8, 8), (4, 3, 2), 2, 1, 1, 2, 0.3, bc=((0, 0), (1, 1), (2, 2)))
+    for rlo, rhi in [((1, 1, 0), (3, 2, 2)), ((0, 0, 0), (0, 0, 0)), ((0, 0, 0), (4, 3, 2))]:
+        assert spark.amr_leaves(p.config(), rlo, rhi) == oracle.amr_leaves(p.config(), rlo, rhi)
+        assert sum(spark.amr_leaves(p.config(), rlo, rhi)) == len(si.amr_leaf_blocks(p, rlo, rhi))
+    with pytest.raises(spark.SparkError):
+        spark.amr_leaves(p.with_(nb=(7, 8, 8)).config(), (1, 1, 0), (3, 2, 2))
+    with pytest.raises(spark.SparkError):
+        spark.amr_leaves(p.config(), (1, 1, 0), (5, 2, 2))
+    import ctypes
+
+    def nbytes(rlo, rhi):
+        n = ctypes.c_size_t()
+        c, r = spark.to_cconfig(p.config()), spark._refine(rlo, rhi)
+        assert spark.lib().spark_amr_required_bytes(ctypes.byref(c), ctypes.byref(r), ctypes.byref(n)) == 0
+        return n.value
+
+    assert nbytes((1, 1, 0), (3, 2, 2)) > nbytes((0, 0, 0), (0, 0, 0))

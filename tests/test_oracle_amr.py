@@ -100,17 +100,18 @@ def test_fill_against_composite_arrays(p, rlo, rhi):
         A = F if lev else C
         NL = [N[d] * (r[d] if lev else 1) for d in range(3)]
         for d in range(p.ndim):
+            tr = [e for e in range(p.ndim) if e != d]  # transverse dimensions
             for side in (0, 1):
                 for depth in range(g[d]):
                     loc_d = -1 - depth if side == 0 else p.nb[d] + depth
-                    for t2 in range(p.nb[(d + 2) % 3] if p.ndim == 3 else 1):
-                        for t1 in range(p.nb[(d + 1) % 3] if p.ndim >= 2 else 1):
+                    for t2 in range(p.nb[tr[1]] if len(tr) > 1 else 1):
+                        for t1 in range(p.nb[tr[0]] if len(tr) > 0 else 1):
                             loc = [0, 0, 0]
                             loc[d] = loc_d
-                            if p.ndim >= 2:
-                                loc[(d + 1) % 3] = t1
-                            if p.ndim == 3:
-                                loc[(d + 2) % 3] = t2
+                            if len(tr) > 0:
+                                loc[tr[0]] = t1
+                            if len(tr) > 1:
+                                loc[tr[1]] = t2
                             gc = [b[e] * p.nb[e] + loc[e] for e in range(3)]
                             gm, flip = mapped(gc[d], NL[d], p.bc[d][0], p.bc[d][1])
                             gc[d] = gm
@@ -123,7 +124,8 @@ def test_fill_against_composite_arrays(p, rlo, rhi):
         # interior copied
         inner = P[:, q, g[2]:g[2] + p.nb[2], g[1]:g[1] + p.nb[1], g[0]:g[0] + p.nb[0]]
         assert np.array_equal(inner, U[:, q])
-    assert checked > 0
+    nface = sum(2 * g[d] * int(np.prod([p.nb[e] for e in range(p.ndim) if e != d])) for d in range(p.ndim))
+    assert checked == nface * nl
 
 
 def test_empty_box_is_the_uniform_coarse_scheme():
