@@ -177,6 +177,74 @@ def problem_for(args, world: int) -> si.Problem:
     return p
 
 
+# ------------------------------------------------------------- N3 (AMR) leg
+def run_amr(args, rank: int, world: int, local: int) -> int:
+    """NEXT N3 measurement: composite SSP-RK steps of the static two-level
+    refinement (fluxBuff + flux correction), the config's coarse grid with the
+    central blocks refined (a quarter of the block grid per dimension, at
+    least one block), synthetic smooth pulse crossing the coarse-fine faces.
+    One GPU (replicas only: the refined path is single-rank).  Zone-updates =
+    leaf cells x RK stages; the roofline denominator is the same algorithmic
+    bytes per zone-update as the uniform path (the unfused N3 kernels move
+    more: padded tiles and face fluxes through HBM)."""
+    import torch
+
+    from paper_2401_03378_b200 import spark
+
+    if rank != 0:
+        return 0
+    torch.cuda.set_device(local)
+    p = problem_for(args, 1)
+    nd = p.ndim
+    q = [max(1, p.nblk[d] // 4) if d < nd else 1 for d in range(3)]
+    rlo = tuple((p.nblk[d] - q[d]) // 2 if d < nd else 0 for d in range(3))
+    rhi = tuple(rlo[d] + q[d] if d < nd else 1 for d in range(3))
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        a = spark.Amr(p.config(), rlo, rhi, device=local, stream=stream)
+        W = si.amr_primitive(p, rlo, rhi, "pulse")
+        nl = W.shape[1]
+        rho, vel, pres = W[0], W[1:1 + nd], W[-1]
+        U = np.empty_like(W)
+        U[0] = rho
+        U[1:1 + nd] = rho * vel
+        U[-1] = pres / (p.gamma - 1.0) + 0.5 * rho * np.sum(vel * vel, axis=0)
+        a.set_state(U)
+    cells = nl * int(np.prod(p.nb))
+    for _ in range(args.warmup):
+        a.step()
+    stream.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            a.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    value = cells * p.rk_stages * args.steps / (ms * 1e-3)
+    peaks, peak_kind = measured_peaks()
+    bps = sum(algorithmic_bytes_per_zone(p, st) for st in range(1, p.rk_stages + 1)) * cells
+    achieved = bps * args.steps / (ms * 1e-3) / 1e9
+    nc, nf = spark.amr_leaves(p.config(), rlo, rhi)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": p.name + "+amr", "coarse_blocks": list(p.nblk), "block": list(p.nb),
+                       "refined_box": [list(rlo), list(rhi)], "leaves": {"coarse": nc, "fine": nf},
+                       "cells": cells, "recon": ["first", "plm", "weno5", "plm_mc", "weno5z"][p.recon],
+                       "riemann": ["hll", "hllc", "hybrid"][p.riemann], "rk_stages": p.rk_stages,
+                       "ic": "smooth pulse crossing the coarse-fine faces", "path": "spark_amr_step (NEXT N3)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                         "kernel": "whole step (unfused N3 kernels)",
+                         "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    a.close()
+    return 0
+
+
 # ---------------------------------------------------------------- oracle leg
 def oracle_sample(p: si.Problem, budget_s: float, max_steps: int = 1000):
     """Time the oracle (as it stands) on a bounded sample of the workload:
@@ -250,6 +318,9 @@ def main():
     ap.add_argument("--shock-thresh", type=float, default=0.5, help="shockDet threshold for --riemann hybrid")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = the config's grid per GPU; strong = the config's grid split over N")
+    ap.add_argument("--amr", action="store_true",
+                    help="NEXT N3: time the static two-level refinement (spark_amr_step) on the config's grid "
+                         "with its central quarter of blocks per dimension refined (one GPU)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -260,6 +331,8 @@ def main():
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.amr:
+        return run_amr(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
