@@ -321,7 +321,8 @@ def main():
     ap.add_argument("--amr", action="store_true",
                     help="NEXT N3: time the static two-level refinement (spark_amr_step) on the config's grid "
                          "with its central quarter of blocks per dimension refined (one GPU)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-calibration", action="store_true")
@@ -475,13 +476,20 @@ def main():
     else:
         hostU = torch.empty(s.shape, dtype=torch.float64).pin_memory()
         s.get_state(out=hostU.numpy())
+        if not (args.telescoping or args.graphs):  # warm-up: copy streams and events created
+            s.step_host(hostU.numpy(), hostU.numpy(), nchunks=args.e2e_chunks)
+            torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        hu = hostU.numpy()
         for _ in range(args.e2e_steps):
-            s.set_state(hostU.numpy())
-            step()
-            s.get_state(out=hostU.numpy())
+            if args.telescoping or args.graphs:  # no host-buffer variant of those steps
+                s.set_state(hu)
+                step()
+                s.get_state(out=hu)
+            else:  # spark_step_host: upload, step, download, the copies pipelined in chunks
+                s.step_host(hu, hu, nchunks=args.e2e_chunks)
         torch.cuda.synchronize()
         barrier()
         el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local}")
@@ -491,7 +499,44 @@ def main():
         nbytes = int(np.prod(s.shape)) * 8
         e2e = {"value": zu_per_step * args.e2e_steps / el, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
-               "note": "per step: spark_set_state from pinned host + spark_step + spark_get_state to pinned host"}
+               "note": ("per step: spark_step_host — the state uploaded from pinned host memory, one step, "
+                        "the new state downloaded to pinned host memory; the copies move in "
+                        f"{args.e2e_chunks} block chunks, the previous step's download overlapping the next upload "
+                        "(full-duplex PCIe); host wall clock around the steps")}
+        # the bound the copies set: pinned host <-> device bandwidth for the
+        # state size, each direction alone and both at once (torch copies on
+        # two streams; the library is not involved)
+        try:
+            dev_buf = torch.empty(s.shape, dtype=torch.float64, device=f"cuda:{local}")
+            host2 = torch.empty(s.shape, dtype=torch.float64).pin_memory()
+            sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+
+            def timed(fn):
+                torch.cuda.synchronize()
+                t = time.perf_counter()
+                fn()
+                torch.cuda.synchronize()
+                return time.perf_counter() - t
+
+            def up():
+                with torch.cuda.stream(sa):
+                    dev_buf.copy_(hostU, non_blocking=True)
+
+            def down():
+                with torch.cuda.stream(sb):
+                    host2.copy_(dev_buf, non_blocking=True)
+
+            timed(up), timed(down)
+            t_up, t_down = timed(up), timed(down)
+            t_both = timed(lambda: (up(), down()))
+            e2e["pcie"] = {"h2d_gbs": nbytes / t_up / 1e9, "d2h_gbs": nbytes / t_down / 1e9,
+                           "bidirectional_gbs": 2 * nbytes / t_both / 1e9,
+                           "bound_zu_per_s": zu_per_step / (t_both + ms * 1e-3 / args.steps),
+                           "note": "copies of the state size; bound = one step's zone-updates / (both "
+                                   "directions at once + the device step time)"}
+            del dev_buf, host2
+        except Exception as exc:  # pragma: no cover - measurement aid only
+            e2e["pcie"] = {"error": str(exc)}
         # simulation-style use of the API: the state stays resident; every step
         # reads its dt back (spark_step with dt_used, a synchronising call), the
         # state is uploaded once before and downloaded once after the K steps

@@ -235,6 +235,19 @@ spark_status spark_step(spark_ctx* ctx, double dt, double t_end, double* dt_used
  * Results are identical to calling spark_step nsteps times. */
 spark_status spark_run(spark_ctx* ctx, int64_t nsteps, double dt, double t_end);
 
+/* One step with the state in HOST memory (end-to-end use; canonical layout,
+ * pinned for asynchronous copies): upload U_in, step (dt, t_end as spark_step;
+ * t and the step count continue — they are not reset as by spark_set_state),
+ * download the new U^n to U_out (may alias U_in).  The transfers move nchunks
+ * block ranges: chunk j of the upload waits only for chunk j of the previous
+ * call's download, so consecutive calls overlap their downloads with the next
+ * uploads (full-duplex PCIe), and each chunk's relayout overlaps the remaining
+ * copies.  Asynchronous: the host buffers must stay valid until the context
+ * stream is synchronised (the stream waits for the last download).  Errors
+ * surface at the next synchronising call. */
+spark_status spark_step_host(spark_ctx* ctx, const double* U_in, double* U_out, double dt, double t_end,
+                             int32_t nchunks);
+
 /* Telescoping SSP-RK step (lst:spark-telescoping
  * P:1598-1604): one guard gather per STEP with S*NGK layers
  * (NGK = reconstruction half-width), then all S stages per block with the halo

@@ -249,6 +249,9 @@ struct spark_ctx {
         double dt = 0.0, t_end = 0.0;
     } graphs[3];
     double prof_ms = 0.0;
+    // spark_step_host: copy streams and per-chunk events (created on first use)
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev_h2d, ev_out, ev_d2h;
 };
 
 namespace {
@@ -661,6 +664,12 @@ spark_status spark_finalize(spark_ctx* ctx) {
         if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
         if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
         if (ctx->ev_recv) cudaEventDestroy(ctx->ev_recv);
+        if (ctx->h2d) CU(cudaStreamSynchronize(ctx->h2d));
+        if (ctx->d2h) CU(cudaStreamSynchronize(ctx->d2h));
+        for (auto* v : {&ctx->ev_h2d, &ctx->ev_out, &ctx->ev_d2h})
+            for (cudaEvent_t e : *v) cudaEventDestroy(e);
+        if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+        if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     });
     if (ctx->group) {
         auto& m = ctx->group->members;
@@ -886,6 +895,83 @@ spark_status spark_step_group(spark_ctx* const* ctxs, int32_t n, double dt, doub
             CU(cudaMemcpy(&h0, &c0->sc->dt, sizeof(double), cudaMemcpyDeviceToHost));
             *dt_used = h0;
         }
+    });
+}
+
+// One step with host buffers, the copies pipelined with the device work:
+// the state is moved in nchunks block ranges; chunk j of the upload waits only
+// for chunk j of the previous call's download (full-duplex PCIe: this call's
+// H2D overlaps the previous call's D2H), its relayout runs as soon as it has
+// arrived; the download of chunk j starts when its relayout out of the new
+// U^n is done.  Staging: canonical copies go through the two state buffers
+// that are dead at that point (in: the stage-1 output buffer before stage 1;
+// out: the buffer after U^(n+1)), chunk by chunk, so no extra memory.
+spark_status spark_step_host(spark_ctx* ctx, const double* U_in, double* U_out, double dt, double t_end,
+                             int32_t nchunks) {
+    if (!ctx || !U_in || !U_out || nchunks < 1) return SPARK_ERR_ARG;
+    return guard(ctx, [&] {
+        if (ctx->group) throw Error(SPARK_ERR_STATE, "local-group contexts step with spark_step_group");
+        set_device(ctx);
+        const spark::Geo& g = ctx->plan.geo;
+        const long long nblk = (long long)g.bn[0] * g.bn[1] * g.bn[2];
+        const int m = (int)std::min<long long>(nchunks, nblk);
+        if (!ctx->h2d) {
+            CU(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+            CU(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+        }
+        while ((int)ctx->ev_h2d.size() < m) {
+            cudaEvent_t a, b, c;
+            CU(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
+            ctx->ev_h2d.push_back(a);
+            ctx->ev_out.push_back(b);
+            ctx->ev_d2h.push_back(c);
+        }
+        auto range = [&](int j, long long* b0, long long* b1) {
+            *b0 = nblk * j / m;
+            *b1 = nblk * (j + 1) / m;
+        };
+        auto segs = [&](cudaStream_t st, const double* src, double* dst, long long b0, long long b1,
+                        cudaMemcpyKind kind) {
+            for (int v = 0; v < g.nvar; v++) {
+                const size_t off = (size_t)v * g.ncell + (size_t)b0 * g.cpb;
+                CU(cudaMemcpyAsync(dst + off, src + off, sizeof(double) * (size_t)(b1 - b0) * g.cpb, kind, st));
+            }
+        };
+        const int n = ctx->n_idx;
+        double* Sin = ctx->U[(n + 1) % 3];
+        // ---- in: H2D chunk j (after the previous call's D2H of chunk j) -> relayout into U^n
+        for (int j = 0; j < m; j++) {
+            long long b0, b1;
+            range(j, &b0, &b1);
+            CU(cudaStreamWaitEvent(ctx->h2d, ctx->ev_d2h[j], 0));
+            segs(ctx->h2d, U_in, Sin, b0, b1, cudaMemcpyHostToDevice);
+            CU(cudaEventRecord(ctx->ev_h2d[j], ctx->h2d));
+            CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_h2d[j], 0));
+            launched(ctx, spark::launch_relayout_range(g, Sin, ctx->U[n], 1, b0, b1, ctx->stream), "relayout");
+        }
+        // ---- the step: CFL minimum of the uploaded U^n (global), then the stages
+        launched(ctx, spark::launch_acc_reset(ctx->sc, ctx->stream), "acc reset");
+        launched(ctx, spark::launch_cfl_min(g, ctx->U[n], ctx->sc, ctx->stream), "cfl min");
+        allreduce_acc(ctx);
+        ctx->have_state = true;
+        launched(ctx, spark::launch_step_begin(ctx->sc, dt, t_end, ctx->cfg.cfl, ctx->stream), "step begin");
+        do_step(ctx, dt);
+        // ---- out: relayout chunk j of U^(n+1) -> D2H chunk j
+        const int nn = ctx->n_idx;
+        double* Sout = ctx->U[(nn + 1) % 3];
+        for (int j = 0; j < m; j++) {
+            long long b0, b1;
+            range(j, &b0, &b1);
+            launched(ctx, spark::launch_relayout_range(g, ctx->U[nn], Sout, 0, b0, b1, ctx->stream), "relayout");
+            CU(cudaEventRecord(ctx->ev_out[j], ctx->stream));
+            CU(cudaStreamWaitEvent(ctx->d2h, ctx->ev_out[j], 0));
+            segs(ctx->d2h, Sout, U_out, b0, b1, cudaMemcpyDeviceToHost);
+            CU(cudaEventRecord(ctx->ev_d2h[j], ctx->d2h));
+        }
+        // a later synchronisation of the context stream covers the downloads
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_d2h[m - 1], 0));
     });
 }
 

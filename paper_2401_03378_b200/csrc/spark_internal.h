@@ -84,6 +84,10 @@ cudaError_t launch_step_begin(DevScalars* sc, double dt_fixed, double t_end, dou
 cudaError_t launch_prim_to_cons(const Geo& g, const double* w, double* u, cudaStream_t s);
 // canonical U[v][b][c] <-> internal U[b][v][c] (to_internal = 1: canonical -> internal)
 cudaError_t launch_relayout(const Geo& g, const double* src, double* dst, int to_internal, cudaStream_t s);
+// blocks [b0, b1) only (chunked host <-> device transfers, spark_step_host)
+cudaError_t launch_relayout_range(const Geo& g, const double* src, double* dst, int to_internal, long long b0,
+                                  long long b1, cudaStream_t s);
+cudaError_t launch_acc_reset(DevScalars* sc, cudaStream_t s);
 cudaError_t launch_pack(const Geo& g, const double* u, int dim, int side, double* slab, cudaStream_t s);
 cudaError_t launch_fill_padded(const Geo& g, const double* u, const double* const halo[3][2], double* padded,
                                cudaStream_t s);

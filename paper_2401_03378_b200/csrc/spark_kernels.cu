@@ -133,11 +133,12 @@ __global__ void prim_to_cons_kernel(const Geo g, const double* __restrict__ w, d
 // (variable, block) chunk of cpb contiguous elements on both sides (16-byte
 // accesses when cpb is even); no index division per element
 __global__ void relayout_kernel(const Geo g, const double* __restrict__ src, double* __restrict__ dst,
-                                int to_internal) {
-    const long long nblk = g.ncell / g.cpb, nchunk = nblk * g.nvar;
+                                int to_internal, long long b0, long long b1) {
+    // blocks [b0, b1) of every variable (the whole state: 0, nblocks)
+    const long long nblk = b1 - b0, nchunk = nblk * g.nvar;
     const bool vec = (g.cpb & 1) == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
     for (long long ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
-        const long long v = ch / nblk, b = ch - v * nblk;
+        const long long v = ch / nblk, b = b0 + ch - v * nblk;
         const long long canon = v * g.ncell + b * g.cpb, inter = b * g.bs + v * g.vs;
         const double* s = src + (to_internal ? canon : inter);
         double* d = dst + (to_internal ? inter : canon);
@@ -249,8 +250,22 @@ cudaError_t launch_prim_to_cons(const Geo& g, const double* w, double* u, cudaSt
 }
 
 cudaError_t launch_relayout(const Geo& g, const double* src, double* dst, int to_internal, cudaStream_t s) {
-    const long long nchunk = g.ncell / g.cpb * g.nvar;
-    relayout_kernel<<<(unsigned)(nchunk < 148LL * 64 ? nchunk : 148LL * 64), 256, 0, s>>>(g, src, dst, to_internal);
+    return launch_relayout_range(g, src, dst, to_internal, 0, g.ncell / g.cpb, s);
+}
+
+cudaError_t launch_relayout_range(const Geo& g, const double* src, double* dst, int to_internal, long long b0,
+                                  long long b1, cudaStream_t s) {
+    const long long nchunk = (b1 - b0) * g.nvar;
+    if (nchunk <= 0) return cudaSuccess;
+    relayout_kernel<<<(unsigned)(nchunk < 148LL * 64 ? nchunk : 148LL * 64), 256, 0, s>>>(g, src, dst, to_internal,
+                                                                                       b0, b1);
+    return cudaGetLastError();
+}
+
+__global__ void acc_reset_kernel(DevScalars* sc) { sc->acc = 0x7ff0000000000000ull; }
+
+cudaError_t launch_acc_reset(DevScalars* sc, cudaStream_t s) {
+    acc_reset_kernel<<<1, 1, 0, s>>>(sc);
     return cudaGetLastError();
 }
 

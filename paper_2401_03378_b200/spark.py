@@ -26,6 +26,7 @@ EXPORTS = [
     "spark_get_time", "spark_get_cfl_min", "spark_fill_guardcells", "spark_step", "spark_advance",
     "spark_step_group", "spark_stage_apply", "spark_profile_enable", "spark_profile_read",
     "spark_selftest_riemann", "spark_axpy", "spark_step_telescoping", "spark_run", "spark_set_time",
+    "spark_step_host",
     "spark_amr_leaves", "spark_amr_required_bytes", "spark_amr_init", "spark_amr_finalize", "spark_amr_last_error",
     "spark_amr_set_state", "spark_amr_get_state", "spark_amr_fill_guardcells", "spark_amr_step", "spark_amr_get_time",
 ]
@@ -124,6 +125,7 @@ def lib() -> ctypes.CDLL:
         "spark_get_time": (i32, [vp, P(d), P(i64), P(d)]),
         "spark_get_cfl_min": (i32, [vp, P(d)]),
         "spark_set_time": (i32, [vp, d, i64]),
+        "spark_step_host": (i32, [vp, vp, vp, d, d, i32]),
         "spark_amr_leaves": (i32, [cp, P(CRefine), P(i64), P(i64)]),
         "spark_amr_required_bytes": (i32, [cp, P(CRefine), P(ctypes.c_size_t)]),
         "spark_amr_init": (i32, [cp, P(CRefine), i32, vp, vp, ctypes.c_size_t, P(vp)]),
@@ -311,6 +313,17 @@ class Spark:
             return d.value
         _check(lib().spark_step(self.ctx, dt, t_end, None), self.ctx, "step")
         return None
+
+    def step_host(self, U_in, U_out, dt: float = 0.0, t_end: float = 0.0, nchunks: int = 8):
+        """One step from host memory to host memory (spark_step_host), with the
+        copies pipelined; asynchronous: both arrays must stay alive (and pinned
+        for overlap) until sync()."""
+        for x in (U_in, U_out):
+            if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags["C_CONTIGUOUS"]
+                    and x.size == int(np.prod(self.shape))):
+                raise ValueError("host state must be a C-contiguous float64 array of the local shape")
+        _check(lib().spark_step_host(self.ctx, ctypes.c_void_p(U_in.ctypes.data), ctypes.c_void_p(U_out.ctypes.data),
+                                     dt, t_end, nchunks), self.ctx, "step_host")
 
     def run(self, nsteps: int, dt: float = 0.0, t_end: float = 0.0):
         """nsteps steps, asynchronous; CUDA-graph replay on a non-default stream."""
