@@ -250,13 +250,33 @@ spark_status spark_step_host(spark_ctx* ctx, const double* U_in, double* U_out, 
 
 /* Telescoping SSP-RK step (lst:spark-telescoping
  * P:1598-1604): one guard gather per STEP with S*NGK layers
- * (NGK = reconstruction half-width), then all S stages per block with the halo
- * area updated too, in ONE kernel (the intermediate stages stay on chip).
- * Guards beyond a physical boundary are filled once and evolved (DESIGN.md
- * reading R17); with periodic boundaries the result equals spark_step.
- * Single-rank contexts, ndim <= 2 (a 3-D tile does not fit on chip); same dt
- * and dt_used semantics as spark_step. */
+ * (NGK = reconstruction half-width; faces, edges and corners), then all S
+ * stages per block with the halo area updated too.  Guards beyond a physical
+ * boundary are filled once and evolved (reading R17); with periodic
+ * boundaries the result equals spark_step.  Same dt and dt_used semantics as
+ * spark_step.
+ * Two implementations: 1-D/2-D single-rank contexts without NCCL run ONE
+ * kernel per step with the tile on chip; 3-D, NCCL contexts (several ranks or
+ * self-exchange) or contexts given a scratch (spark_set_scratch) keep the
+ * tiles in HBM: the rank's S*NGK-thick shell (26 regions: faces, edges,
+ * corners) is exchanged ONCE per step (one grouped NCCL call), then gather +
+ * S stage passes.  The result of a block is bitwise independent of the rank
+ * count.  The HBM path needs spark_set_scratch first. */
 spark_status spark_step_telescoping(spark_ctx* ctx, double dt, double t_end, double* dt_used);
+
+/* Device bytes of the scratch the HBM telescoping path needs (three tiles of
+ * U, the primitive tile, the face fluxes and the 2 x 26 shell buffers). */
+spark_status spark_telescoping_scratch_bytes(const spark_config* cfg, int32_t rank, int32_t nranks, size_t* bytes);
+
+/* Give the context a caller-owned scratch (device, 256-byte aligned, >= the
+ * bytes above) for the HBM telescoping path; selects that path for every
+ * spark_step_telescoping of this context. */
+spark_status spark_set_scratch(spark_ctx* ctx, void* scratch, size_t bytes);
+
+/* spark_step_telescoping for the contexts of one spark_init_local_group (each
+ * with a scratch): one shell exchange between the virtual ranks per step. */
+spark_status spark_step_group_telescoping(spark_ctx* const* ctxs, int32_t n, double dt, double t_end,
+                                          double* dt_used);
 
 /* Enqueue up to max_steps steps (CFL dt, clipped to t_end), synchronising
  * every check_every steps (<= 0: only at the end) to stop once t_end is

@@ -249,6 +249,15 @@ struct spark_ctx {
         double dt = 0.0, t_end = 0.0;
     } graphs[3];
     double prof_ms = 0.0;
+    // telescoping through HBM tiles (3-D / multi-rank): caller-owned scratch
+    struct Tiles {
+        spark::TileGeo tg{};
+        double *T0 = nullptr, *Ta = nullptr, *Tb = nullptr, *W = nullptr, *F = nullptr;
+        double* send[27] = {};
+        double* recv[27] = {};
+        int peer[27];
+        bool ready = false;
+    } tiles;
     // spark_step_host: copy streams and per-chunk events (created on first use)
     cudaStream_t h2d = nullptr, d2h = nullptr;
     std::vector<cudaEvent_t> ev_h2d, ev_out, ev_d2h;
@@ -519,6 +528,167 @@ void do_step(spark_ctx* c, double dt) {
     }
     allreduce_acc(c);
     c->n_idx = newn;
+}
+
+// ------------------------------------------------ telescoping through tiles
+spark::TileGeo tile_geo(const spark_config* c, const Plan& p) {
+    spark::TileGeo t{};
+    t.g = p.geo;
+    t.ngk = stencil_ng(c->recon);
+    t.S = c->rk_stages;
+    t.G = t.S * t.ngk;
+    t.recon = c->recon;
+    t.np = 1;
+    for (int d = 0; d < 3; d++) {
+        t.pn[d] = c->nb[d] + (d < c->ndim ? 2 * t.G : 0);
+        t.np *= t.pn[d];
+    }
+    long long off = 0;
+    for (int d = 0; d < 3; d++) {
+        t.Fo[d] = off;
+        if (d < c->ndim) {
+            long long f = 1;
+            for (int e = 0; e < 3; e++) f *= t.pn[e] + (e == d ? 1 : 0);
+            off += f;
+        }
+    }
+    t.NF = off;
+    return t;
+}
+
+int dir_of(int c0, int c1, int c2) { return (c0 + 1) + 3 * (c1 + 1) + 9 * (c2 + 1); }
+
+// rank in direction (c0, c1, c2) of the process grid, -1 where a component
+// crosses a side without a peer (physical boundary / local periodic wrap)
+int tile_peer(const Plan& p, int dir) {
+    const int c[3] = {dir % 3 - 1, (dir / 3) % 3 - 1, dir / 9 - 1};
+    int q[3] = {p.pc[0], p.pc[1], p.pc[2]};
+    for (int d = 0; d < 3; d++) {
+        if (!c[d]) continue;
+        if (p.peer[d][c[d] > 0 ? 1 : 0] < 0) return -1;
+        q[d] = ((q[d] + c[d]) % p.pg[d] + p.pg[d]) % p.pg[d];
+    }
+    return q[0] + p.pg[0] * (q[1] + p.pg[1] * q[2]);
+}
+
+size_t tile_scratch_bytes(const spark_config* c, const Plan& p) {
+    const spark::TileGeo t = tile_geo(c, p);
+    const long long nblk = (long long)p.geo.bn[0] * p.geo.bn[1] * p.geo.bn[2];
+    const size_t tile = align_up(sizeof(double) * p.geo.nvar * nblk * t.np);
+    size_t b = 4 * tile + align_up(sizeof(double) * p.geo.nvar * nblk * t.NF);
+    for (int dir = 0; dir < 27; dir++)
+        if (dir != 13 && tile_peer(p, dir) >= 0)
+            b += 2 * align_up(sizeof(double) * p.geo.nvar * spark::tile_region_cells(t, dir));
+    return b;
+}
+
+std::string tile_check(const spark_config* c, const Plan& p) {
+    const int G = c->rk_stages * stencil_ng(c->recon);
+    for (int d = 0; d < c->ndim; d++) {
+        if (G > p.geo.gN[d]) return "telescoped halo deeper than the domain";
+        if ((p.peer[d][0] >= 0 || p.peer[d][1] >= 0) && G > p.geo.cn[d])
+            return "telescoped halo deeper than a rank's sub-box";
+    }
+    return "";
+}
+
+void tile_attach(spark_ctx* c, void* scratch, size_t bytes) {
+    const size_t need = tile_scratch_bytes(&c->cfg, c->plan);
+    if (!scratch) throw Error(SPARK_ERR_ARG, "null scratch");
+    if (bytes < need) throw Error(SPARK_ERR_OOM, "scratch smaller than spark_telescoping_scratch_bytes");
+    if (reinterpret_cast<uintptr_t>(scratch) % 256) throw Error(SPARK_ERR_ARG, "scratch must be 256-byte aligned");
+    auto& T = c->tiles;
+    T.tg = tile_geo(&c->cfg, c->plan);
+    const long long nblk = (long long)c->plan.geo.bn[0] * c->plan.geo.bn[1] * c->plan.geo.bn[2];
+    const size_t tile = align_up(sizeof(double) * c->plan.geo.nvar * nblk * T.tg.np);
+    char* p = static_cast<char*>(scratch);
+    T.T0 = reinterpret_cast<double*>(p), p += tile;
+    T.Ta = reinterpret_cast<double*>(p), p += tile;
+    T.Tb = reinterpret_cast<double*>(p), p += tile;
+    T.W = reinterpret_cast<double*>(p), p += tile;
+    T.F = reinterpret_cast<double*>(p), p += align_up(sizeof(double) * c->plan.geo.nvar * nblk * T.tg.NF);
+    for (int dir = 0; dir < 27; dir++) {
+        T.peer[dir] = dir == 13 ? -1 : tile_peer(c->plan, dir);
+        T.send[dir] = T.recv[dir] = nullptr;
+        if (T.peer[dir] < 0) continue;
+        const size_t rb = align_up(sizeof(double) * c->plan.geo.nvar * spark::tile_region_cells(T.tg, dir));
+        T.send[dir] = reinterpret_cast<double*>(p), p += rb;
+        T.recv[dir] = reinterpret_cast<double*>(p), p += rb;
+    }
+    T.ready = true;
+}
+
+void tile_pack(spark_ctx* c) {
+    auto& T = c->tiles;
+    for (int dir = 0; dir < 27; dir++)
+        if (T.peer[dir] >= 0)
+            launched(c, spark::launch_tile_pack(T.tg, c->U[c->n_idx], dir, T.send[dir], c->stream), "tile pack");
+}
+
+// the shell exchange of one rank over NCCL, ONE grouped call per step.  Both
+// sides order the messages between a pair of ranks by the receiver's
+// direction: my receives by my direction D, my sends by 26 - D (the peer
+// stores what I send for D as its direction 26 - D).
+void tile_exchange_nccl(spark_ctx* c) {
+    auto& T = c->tiles;
+    const spark::Geo& g = c->plan.geo;
+    NC(ncclGroupStart());
+    for (int k = 0; k < 27; k++) {
+        const int rd = k, sd = 26 - k;
+        if (T.peer[rd] >= 0)
+            NC(ncclRecv(T.recv[rd], (size_t)g.nvar * spark::tile_region_cells(T.tg, rd), ncclFloat64, T.peer[rd],
+                        c->comm, c->stream));
+        if (T.peer[sd] >= 0)
+            NC(ncclSend(T.send[sd], (size_t)g.nvar * spark::tile_region_cells(T.tg, sd), ncclFloat64, T.peer[sd],
+                        c->comm, c->stream));
+    }
+    NC(ncclGroupEnd());
+}
+
+void tile_exchange_local(const std::vector<spark_ctx*>& m) {
+    for (spark_ctx* c : m) {
+        auto& T = c->tiles;
+        for (int dir = 0; dir < 27; dir++) {
+            if (T.peer[dir] < 0) continue;
+            spark_ctx* q = m[T.peer[dir]];
+            const size_t bytes = sizeof(double) * c->plan.geo.nvar * spark::tile_region_cells(T.tg, dir);
+            CU(cudaMemcpyAsync(T.recv[dir], q->tiles.send[26 - dir], bytes, cudaMemcpyDeviceToDevice, c->stream));
+        }
+    }
+}
+
+// gather + the S stages of one rank; writes U^(n+1) into U[(n+1)%3]
+void tile_stages(spark_ctx* c) {
+    auto& T = c->tiles;
+    spark::ShellPtrs sh{};
+    for (int dir = 0; dir < 27; dir++) sh.p[dir] = T.recv[dir];
+    const int n = c->n_idx, out = (n + 1) % 3;
+    cudaEvent_t e1 = nullptr;
+    if (c->prof) {  // the gather + stage passes count as the step's stage-kernel time
+        if (c->ev_used == c->ev.size()) {
+            cudaEvent_t x, y;
+            CU(cudaEventCreate(&x));
+            CU(cudaEventCreate(&y));
+            c->ev.emplace_back(x, y);
+        }
+        CU(cudaEventRecord(c->ev[c->ev_used].first, c->stream));
+        e1 = c->ev[c->ev_used].second;
+        c->ev_used++;
+    }
+    launched(c, spark::launch_tile_gather(T.tg, c->U[n], sh, T.T0, c->stream), "tile gather");
+    const int S = c->cfg.rk_stages;
+    const double* prev = T.T0;
+    for (int s = 1; s <= S; s++) {
+        double a, b;
+        rk_coeffs(S, s, &a, &b);
+        double* tout = (s & 1) ? T.Ta : T.Tb;
+        launched(c, spark::launch_tile_stage(T.tg, c->cfg.riemann, prev, T.T0, T.W, T.F, tout, c->U[out], a, b, s,
+                                             s == S ? 1 : 0, c->sc, c->stream),
+                 "tile stage");
+        prev = tout;
+    }
+    if (e1) CU(cudaEventRecord(e1, c->stream));
+    c->stage_launches++;
 }
 
 }  // namespace
@@ -1075,13 +1245,91 @@ extern "C" spark_status spark_axpy(int32_t device, int32_t variant, int64_t n, d
     });
 }
 
+extern "C" spark_status spark_telescoping_scratch_bytes(const spark_config* cfg, int32_t rank, int32_t nranks,
+                                                       size_t* bytes) {
+    return guard(nullptr, [&] {
+        if (!bytes) throw Error(SPARK_ERR_ARG, "null bytes");
+        Plan p = make_plan(cfg, rank, nranks, nranks == 1);
+        *bytes = tile_scratch_bytes(cfg, p);
+    });
+}
+
+extern "C" spark_status spark_set_scratch(spark_ctx* ctx, void* scratch, size_t bytes) {
+    if (!ctx) return SPARK_ERR_ARG;
+    return guard(ctx, [&] { tile_attach(ctx, scratch, bytes); });
+}
+
+// telescoping step through HBM tiles (one shell exchange per step)
+static void tile_step_one(spark_ctx* ctx, double dt, double t_end) {
+    std::string m = tile_check(&ctx->cfg, ctx->plan);
+    if (!m.empty()) throw Error(SPARK_ERR_ARG, m);
+    if (!ctx->tiles.ready) throw Error(SPARK_ERR_STATE, "telescoping tiles need spark_set_scratch first");
+    launched(ctx, spark::launch_step_begin(ctx->sc, dt, t_end, ctx->cfg.cfl, ctx->stream), "step begin");
+    tile_pack(ctx);
+    if (ctx->comm) tile_exchange_nccl(ctx);
+    tile_stages(ctx);
+    allreduce_acc(ctx);
+    ctx->n_idx = (ctx->n_idx + 1) % 3;
+}
+
+extern "C" spark_status spark_step_group_telescoping(spark_ctx* const* ctxs, int32_t n, double dt, double t_end,
+                                                     double* dt_used) {
+    if (!ctxs || n < 1 || !ctxs[0]) return SPARK_ERR_ARG;
+    spark_ctx* c0 = ctxs[0];
+    return guard(c0, [&] {
+        if (!c0->group || (int)c0->group->members.size() != n)
+            throw Error(SPARK_ERR_ARG, "needs all contexts of one local group");
+        std::vector<spark_ctx*> m(c0->group->members);
+        for (spark_ctx* c : m) {
+            if (!c->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
+            if (!c->tiles.ready) throw Error(SPARK_ERR_STATE, "telescoping tiles need spark_set_scratch first");
+            std::string msg = tile_check(&c->cfg, c->plan);
+            if (!msg.empty()) throw Error(SPARK_ERR_ARG, msg);
+        }
+        set_device(c0);
+        group_min(m);
+        std::vector<int> old(n);
+        for (int r = 0; r < n; r++) {
+            old[r] = m[r]->n_idx;
+            launched(m[r], spark::launch_step_begin(m[r]->sc, dt, t_end, m[r]->cfg.cfl, m[r]->stream), "step begin");
+            tile_pack(m[r]);
+        }
+        tile_exchange_local(m);  // the one exchange of the step
+        for (spark_ctx* c : m) tile_stages(c);
+        group_min(m);
+        for (spark_ctx* c : m) c->n_idx = (c->n_idx + 1) % 3;
+        if (dt_used) {
+            std::vector<spark::DevScalars> h(n);
+            for (int r = 0; r < n; r++) h[r] = read_scalars(m[r]);
+            if (h[0].bad != spark::kNoBad) {
+                const bool now = failed_now(h[0]);
+                if (now)
+                    for (int r = 0; r < n; r++) rollback(m[r], h[r], old[r]);
+                throw_nonphysical(h[0], now);
+            }
+            *dt_used = h[0].dt;
+        }
+    });
+}
+
 extern "C" spark_status spark_step_telescoping(spark_ctx* ctx, double dt, double t_end, double* dt_used) {
     if (!ctx) return SPARK_ERR_ARG;
     return guard(ctx, [&] {
         if (!ctx->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
-        if (ctx->nranks != 1 || ctx->comm || ctx->group)
-            throw Error(SPARK_ERR_STATE, "telescoping steps need a single-rank context");
-        if (ctx->cfg.ndim > 2) throw Error(SPARK_ERR_ARG, "telescoping steps support ndim <= 2");
+        if (ctx->group) throw Error(SPARK_ERR_STATE, "local-group contexts step with spark_step_group_telescoping");
+        if (ctx->cfg.ndim > 2 || ctx->nranks != 1 || ctx->comm || ctx->tiles.ready) {
+            // 3-D, several ranks, or tiles requested: telescoping through HBM tiles
+            set_device(ctx);
+            const int old_n = ctx->n_idx;
+            tile_step_one(ctx, dt, t_end);
+            if (dt_used) {
+                sync_and_check(ctx, true, old_n);
+                double h;
+                CU(cudaMemcpy(&h, &ctx->sc->dt, sizeof(double), cudaMemcpyDeviceToHost));
+                *dt_used = h;
+            }
+            return;
+        }
         const int S = ctx->cfg.rk_stages;
         const int ngk = stencil_ng(ctx->cfg.recon);
         for (int d = 0; d < ctx->cfg.ndim; d++)

@@ -71,6 +71,20 @@ struct StageArgs {
                                   // ("interior", run while halos travel); 2 the others
 };
 
+// Telescoping through HBM tiles (spark_telescope_tile.cu): G = S*NGK guard
+// layers per block tile, pn = nb + 2G along the used dims.
+struct TileGeo {
+    Geo g;
+    int G, S, ngk, recon;
+    int pn[3];
+    long long np;                 // cells per tile
+    long long Fo[3], NF;          // face blocks per tile: offsets, total
+};
+// the 26 received shell regions of a rank, by direction (c0+1) + 3(c1+1) + 9(c2+1)
+struct ShellPtrs {
+    const double* p[27];
+};
+
 constexpr int kMaxGroup = 64;
 struct AccPtrs {
     unsigned long long* p[kMaxGroup];
@@ -101,5 +115,11 @@ size_t stage_smem_bytes(const Geo& g, int recon);
 size_t telescope_smem_bytes(const Geo& g, int recon, int S);
 cudaError_t launch_telescope(const StageArgs& a, int recon, int riemann, int S, cudaStream_t s);
 int stage_block_threads(const Geo& g, int recon);
+long long tile_region_cells(const TileGeo& t, int dir);
+cudaError_t launch_tile_pack(const TileGeo& t, const double* u, int dir, double* buf, cudaStream_t s);
+cudaError_t launch_tile_gather(const TileGeo& t, const double* u, const ShellPtrs& sh, double* T0, cudaStream_t s);
+cudaError_t launch_tile_stage(const TileGeo& t, int riemann, const double* Tprev, const double* T0, double* W,
+                              double* F, double* Tout, double* uout, double a, double b, int s, int last,
+                              DevScalars* sc, cudaStream_t st);
 
 }  // namespace spark

@@ -26,7 +26,7 @@ EXPORTS = [
     "spark_get_time", "spark_get_cfl_min", "spark_fill_guardcells", "spark_step", "spark_advance",
     "spark_step_group", "spark_stage_apply", "spark_profile_enable", "spark_profile_read",
     "spark_selftest_riemann", "spark_axpy", "spark_step_telescoping", "spark_run", "spark_set_time",
-    "spark_step_host",
+    "spark_step_host", "spark_telescoping_scratch_bytes", "spark_set_scratch", "spark_step_group_telescoping",
     "spark_amr_leaves", "spark_amr_required_bytes", "spark_amr_init", "spark_amr_finalize", "spark_amr_last_error",
     "spark_amr_set_state", "spark_amr_get_state", "spark_amr_fill_guardcells", "spark_amr_step", "spark_amr_get_time",
 ]
@@ -126,6 +126,9 @@ def lib() -> ctypes.CDLL:
         "spark_get_cfl_min": (i32, [vp, P(d)]),
         "spark_set_time": (i32, [vp, d, i64]),
         "spark_step_host": (i32, [vp, vp, vp, d, d, i32]),
+        "spark_telescoping_scratch_bytes": (i32, [cp, i32, i32, P(ctypes.c_size_t)]),
+        "spark_set_scratch": (i32, [vp, vp, ctypes.c_size_t]),
+        "spark_step_group_telescoping": (i32, [P(vp), i32, d, d, P(d)]),
         "spark_amr_leaves": (i32, [cp, P(CRefine), P(i64), P(i64)]),
         "spark_amr_required_bytes": (i32, [cp, P(CRefine), P(ctypes.c_size_t)]),
         "spark_amr_init": (i32, [cp, P(CRefine), i32, vp, vp, ctypes.c_size_t, P(vp)]),
@@ -255,6 +258,8 @@ class Spark:
         self.device = torch.cuda.current_device() if device is None else device
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.shape = local_shape(cfg, rank, nranks)
+        self.nccl = False
+        self.scratch = None
         if _handle is not None:
             self.ctx, self.arena = _handle, _arena
             return
@@ -263,6 +268,7 @@ class Spark:
         c = to_cconfig(cfg)
         h = ctypes.c_void_p()
         idp = None
+        self.nccl = nccl_id is not None
         if nccl_id is not None:
             idp = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
         _check(lib().spark_init(ctypes.byref(c), rank, nranks, idp, self.device,
@@ -314,6 +320,17 @@ class Spark:
         _check(lib().spark_step(self.ctx, dt, t_end, None), self.ctx, "step")
         return None
 
+    def enable_tiles(self):
+        """Allocate the HBM-tile scratch (torch-owned) and select the tile
+        telescoping path (3-D / multi-rank; spark_set_scratch)."""
+        c = to_cconfig(self.cfg)
+        n = ctypes.c_size_t()
+        _check(lib().spark_telescoping_scratch_bytes(ctypes.byref(c), self.rank, self.nranks, ctypes.byref(n)),
+               what="telescoping_scratch_bytes")
+        self.scratch = self.torch.empty(max(n.value, 256), dtype=self.torch.uint8, device=f"cuda:{self.device}")
+        _check(lib().spark_set_scratch(self.ctx, ctypes.c_void_p(self.scratch.data_ptr()), n.value), self.ctx,
+               "set_scratch")
+
     def step_host(self, U_in, U_out, dt: float = 0.0, t_end: float = 0.0, nchunks: int = 8):
         """One step from host memory to host memory (spark_step_host), with the
         copies pipelined; asynchronous: both arrays must stay alive (and pinned
@@ -330,7 +347,11 @@ class Spark:
         _check(lib().spark_run(self.ctx, nsteps, dt, t_end), self.ctx, "run")
 
     def step_telescoping(self, dt: float = 0.0, t_end: float = 0.0, sync: bool = False):
-        """One telescoping SSP-RK step (1-D/2-D, single rank)."""
+        """One telescoping SSP-RK step: on chip for 1-D/2-D single-rank contexts,
+        through HBM tiles (scratch allocated on first use) for 3-D, NCCL
+        contexts, or after enable_tiles()."""
+        if getattr(self, "scratch", None) is None and (self.cfg["ndim"] == 3 or self.nranks > 1 or self.nccl):
+            self.enable_tiles()
         if sync:
             d = ctypes.c_double()
             _check(lib().spark_step_telescoping(self.ctx, dt, t_end, ctypes.byref(d)), self.ctx, "step_telescoping")
@@ -425,6 +446,18 @@ class LocalGroup:
         d = ctypes.c_double()
         _check(lib().spark_step_group(self._handles, len(self.ranks), dt, t_end, ctypes.byref(d) if sync else None),
                self.ranks[0].ctx, "step_group")
+        return d.value if sync else None
+
+    def step_telescoping(self, dt: float = 0.0, t_end: float = 0.0, sync: bool = False):
+        """Telescoping step of the group (one shell exchange per step); the
+        members' tile scratch is allocated on first use."""
+        for r in self.ranks:
+            if getattr(r, "scratch", None) is None:
+                r.enable_tiles()
+        d = ctypes.c_double()
+        _check(lib().spark_step_group_telescoping(self._handles, len(self.ranks), dt, t_end,
+                                                  ctypes.byref(d) if sync else None),
+               self.ranks[0].ctx, "step_group_telescoping")
         return d.value if sync else None
 
     def close(self):

@@ -81,9 +81,10 @@ def test_c3_telescoping_reduced(sp):
     assert_parity(s.get_state().cpu().numpy(), Uo, what="c3 telescoping")
 
 
-def test_telescoping_rejects_3d(sp):
+def test_telescoping_3d_needs_a_scratch(sp):
+    """3-D telescoping runs through HBM tiles (tests/test_gpu_telescoping3d.py);
+    at the ABI, without spark_set_scratch the call is refused (SPARK_ERR_STATE)."""
     p = si.PRESETS["c4_sedov3d_plm"].with_(nblk=(2, 2, 2))
     s = sp.Spark(p.config())
     s.set_primitive(si.initial_primitive(p))
-    with pytest.raises(sp.SparkError):
-        s.step_telescoping()
+    assert sp.lib().spark_step_telescoping(s.ctx, 0.0, 0.0, None) == sp.SPARK_ERR_STATE
