@@ -396,9 +396,6 @@ __host__ __device__ __forceinline__ bool shock_cell(double um, double up, double
 // face between cells i and i+1 from (u, p, rho) of the cells i-1, i, i+1, i+2
 __host__ __device__ __forceinline__ bool shock_face(const double* u, const double* p, const double* r, double thr,
                                                     double gamma) {
-#ifdef EXP_SHK_ALL
-    return true;
-#endif
     return shock_cell(u[0], u[2], p[0], p[2], r[0], r[2], thr, gamma) |
            shock_cell(u[1], u[3], p[1], p[3], r[1], r[3], thr, gamma);
 }

@@ -38,22 +38,10 @@ using namespace dev;
 constexpr int kThreads = 256;
 
 // Launch policy of a specialisation (host and device agree through this).
-//   stage_ops: the S4 operands U^(s-1), U^n of the plane are copied to shared
-//   memory with cp.async, so no registers are held across S2/S3 (3-D PLM and
-//   first order: their shared-memory budget leaves room for the 20 KiB; WENO5
-//   does not and prefetches into registers).
-// (A 9th "boundary" warp doing all halo work was measured slower in 2-D and
-// 3-D — register cap 112 and a serial boundary critical path — DESIGN.md §4.2.)
-//   Superseded by the L2 prefetch of the operands (L2PF below): without the
-//   20 KiB staging buffer a 3-D PLM CTA needs 76 instead of 96 KiB of shared
-//   memory, which leaves the SM a larger L1 (+1 %); kept as an experiment.
-__host__ __device__ constexpr bool policy_stage_ops(int ndim, int recon, int nbx, int nby) {
-#ifdef EXP_STG
-    return nbx == 16 && nby == 16 && ndim == 3 && (recon <= 1 || recon == 3);
-#else
-    return false;
-#endif
-}
+// The design experiments that were measured and dropped (a 9th "boundary"
+// warp, cp.async / TMA staging of the S4 operands, paired face-centric
+// solves, 3 CTAs/SM, ...) are recorded with their numbers in DESIGN.md §4.2;
+// the kernel below keeps only the measured winners.
 // Face-centric x/y reconstruction (16x16 planes, first order / minmod PLM): the
 // thread that solves a face reconstructs both of its states straight from the
 // plane (two limiter evaluations per face instead of one per cell), so the
@@ -85,35 +73,15 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // separate plane (5 LDS + 5 STS per cell and plane).  WENO5's 5 slots would
 // not fit twice per SM; it keeps the compact ring and a separate plane.
 __host__ __device__ constexpr bool policy_pad_ring(int ndim, int recon) {
-#ifdef EXP_NOPADRING
-    return false;
-#else
     return ndim == 3 && recon != 2 && recon != 4;
-#endif
 }
 
-#ifndef EXP_MINB3D
-#define EXP_MINB3D 2
-#endif
 template <int NDIM, int RECON, int RS, int NBX, int NBY, int NBZ>
-__global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_kernel(const StageArgs A) {
-    constexpr bool STAGE_OPS = policy_stage_ops(NDIM, RECON, NBX, NBY);
-#ifdef EXP_NOFC
-    constexpr bool FC = false;
-#else
+__global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(const StageArgs A) {
     constexpr bool FC = policy_face_centric(NDIM, RECON, NBX, NBY);
-#endif
-    // paired face solves in S3 (WENO5 / first order); the face-centric path
-    // solves one face at a time (its reconstruction temporaries would spill)
-#ifdef EXP_NOFUSE
-    constexpr bool FUSE = false;
-#else
-#ifdef EXP_FCFUSE
-    constexpr bool FUSE = NBX == 16 && NBY == 16 && NDIM == 3;
-#else
+    // paired face solves in S3 (WENO5 / MC); the face-centric path solves one
+    // face at a time (paired, its reconstruction temporaries spill: -9 %)
     constexpr bool FUSE = NBX == 16 && NBY == 16 && NDIM == 3 && !FC;
-#endif
-#endif
     constexpr int NV = NDIM + 2;
     constexpr int NG = StencilOf<RECON>::NG;
     constexpr int R = NG - 1;  // cell-centric reconstruction radius
@@ -125,22 +93,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     // 8.9 G zone-updates/s) and no shared-memory staging is needed (PLM +1 %
     // over cp.async staging); 2-D measured 3 % slower that way and keeps the
     // register prefetch
-#ifdef EXP_NO_L2PF
-    constexpr bool L2PF = false;
-#else
-    constexpr bool L2PF = !STAGE_OPS && NDIM == 3;
-#endif
+    constexpr bool L2PF = NDIM == 3;
     // own x / y face fluxes kept in registers for S4 (face-centric 16x16 path)
-#ifdef EXP_NO_OWNF
-    constexpr bool OWNF = false;
-#else
     constexpr bool OWNF = FC && !FUSE && NBX == 16 && NBY == 16 && NDIM >= 2;  // +0.5 %
-#endif
-#ifdef EXP_ZTOP_ALL
-    constexpr bool ZTOP = true;
-#else
     constexpr bool ZTOP = !PADRING;  // z edges of cell k+1 in S1 (see there)
-#endif
     constexpr int RO = NDIM >= 2 ? NG : 0;  // row offset of the interior in cur
     const Geo& g = A.g;
     extern __shared__ double smem[];
@@ -173,15 +129,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     double* XB = XA + NV * fxn;                // [NV][fxn]: R state at x face (not with FC)
     double* YA = XB + (FC ? 0 : NV * fxn);     // [NV][fyn]
     double* YB = YA + NV * fyn;                // [NV][fyn] (not with FC)
-    double* stg = YB + (FC ? 0 : NV * fyn);    // [2][NV][P] staged S4 operands (STAGE_OPS)
     // FC in 3-D: the next plane's raw halo cells arrive by cp.async in shared
     // memory (no prefetch registers held across the plane)
     constexpr bool HSM = FC && NDIM == 3;
-    double* hs = stg + (STAGE_OPS ? 2 * NV * P : 0);  // [NV][nh]
-#ifdef ABL_NOHALO
-    for (int q = threadIdx.x; q < (PADRING ? RING : 1) * NV * CP; q += blockDim.x) (PADRING ? ring : cur0)[q] = 1.0;
-    __syncthreads();
-#endif
+    double* hs = YB + (FC ? 0 : NV * fyn);     // [NV][nh]
 
     const double dt = A.dt_ptr ? *A.dt_ptr : A.dt_value;
     const double a = A.a, bco = A.b;
@@ -282,12 +233,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     // when face z+1/2 is solved)
     auto zshock_cell = [&](int z) -> bool {
         if constexpr (RS != 2) return false;
-#ifdef EXP_SHK_ALL
-        else return true;
-#else
         else return shock_cell(ring_at(z - 1, NV - 2), ring_at(z + 1, NV - 2), ring_at(z - 1, NV - 1),
                                ring_at(z + 1, NV - 1), ring_at(z - 1, 0), ring_at(z + 1, 0), thr, gamma);
-#endif
     };
     bool zs_prev = false;  // shock cell flag of the current plane (z)
     // shockDet at an x or y face (RS 2): c = cell i+1 of the face (variable 0
@@ -359,16 +306,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
     // has no halo work and the S1->S2 barrier no imbalance.  The cp.async of
     // that halo was issued one plane earlier and completed by the previous S4's
     // wait (measured: start of S2 +3.6 % over end of S3).
-#ifdef EXP_NOHLATE
-    constexpr bool HLATE = false;
-#else
     constexpr bool HLATE = HSM && PADRING;
-#endif
-#ifdef ABL_NOHALO
-    const bool hact = false;
-#else
     const bool hact = HPF && (HLATE ? tid >= P - nh : tid < nh);
-#endif
     const int hid = HLATE ? tid - (P - nh) : tid;  // halo cell of this thread
     int hcx = 0, hcy = 0;
     double hpre[NV];
@@ -519,22 +458,13 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
         double u0v[NV], unv[NV];
         const long long cidx = bbase + ((long long)kk * nb1 + tj) * nb0 + ti;
         if (live) {
-            if (STAGE_OPS) {
-#pragma unroll
-                for (int v = 0; v < NV; v++) {
-                    cp_async8(stg + v * P + tid, up + v * vs + cidx);
-                    if (a != 0.0) cp_async8(stg + (NV + v) * P + tid, A.un + v * vs + cidx);
-                }
-                cp_async_commit();
-            } else if (L2PF) {  // only an L2 prefetch now; loaded in S4 (no registers held)
-#pragma unroll
+            if (L2PF) {  // only an L2 prefetch now; loaded in S4 (no registers held)
                 // U^(s-1) of this plane is still in L2 (read as the column
                 // prefetch NG planes ago): only U^n is prefetched (+1.2 % PLM,
                 // +1.8 % WENO5 over prefetching both)
-#ifndef EXP_NOPF_UN
+#pragma unroll
                 for (int v = 0; v < NV; v++)
                     if (a != 0.0) asm volatile("prefetch.global.L2 [%0];" ::"l"(A.un + v * vs + cidx));
-#endif
             } else {
 #pragma unroll
                 for (int v = 0; v < NV; v++) {
@@ -565,9 +495,6 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
         }
         // edge states from the halo cells: one (cell, variable) item per thread
         // round so the extra work spreads over all warps
-#ifdef ABL_NOEDGE
-        if (false)
-#endif
         for (int qv = tid; !FC && qv < nbr * NV; qv += blockDim.x) {
             const int v = qv / nbr, q = qv - v * nbr;
             const bool xd = q < 2 * nb1;
@@ -706,11 +633,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     }
                 }
             }
-#ifdef ABL_NOBND
-            if (false) {
-#else
             if (tid < 32) {  // warp 0: boundary face (+ its z faces)
-#endif
                 const bool isy = tid >= 16;
                 const int q = tid & 15;
                 double bl[NV], br[NV], fb[NV];
@@ -776,11 +699,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                 if (FC && NBX == 16 && NBY == 16) {
                     // warp 0: the 32 block-boundary faces in one pass (y faces in the
                     // x frame with u_x <-> u_y swapped, bitwise identical; see FUSE)
-#ifdef ABL_NOBND
-                    if (false) {
-#else
                     if (tid < 32) {
-#endif
                         const bool isy = tid >= 16;
                         const int q = tid & 15;
                         double bl[NV], br[NV], fb[NV];
@@ -848,7 +767,6 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     else Lv[v] = -(dfx + dfy) - (fzhi[v] - fzlo[v]) * g.rdx[2];
                 }
             }
-            if (STAGE_OPS) cp_async_wait_all();  // operands (and, HLATE, the next halo)
             if (L2PF) {
 #pragma unroll
                 for (int v = 0; v < NV; v++) {
@@ -856,16 +774,15 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? EXP_MINB3D : 3) stage_ke
                     unv[v] = a != 0.0 ? __ldg(A.un + v * vs + cidx) : 0.0;
                 }
             }
-            auto op_u0 = [&](int v) { return STAGE_OPS ? stg[v * P + tid] : u0v[v]; };
             if (g.has_grav) {  // grvAccel source at U^(s-1) (CTA-uniform branch)
                 double grho = 0.0, gmg = 0.0;
 #pragma unroll
-                for (int v = 0; v < NV; v++) Lv[v] += grav_src<NV>(g, v, op_u0(v), grho, gmg);
+                for (int v = 0; v < NV; v++) Lv[v] += grav_src<NV>(g, v, u0v[v], grho, gmg);
             }
 #pragma unroll
             for (int v = 0; v < NV; v++) {
-                const double u0 = op_u0(v);
-                const double unn = STAGE_OPS ? (a != 0.0 ? stg[(NV + v) * P + tid] : 0.0) : unv[v];
+                const double u0 = u0v[v];
+                const double unn = unv[v];
                 const double uo = fma(bco, fma(dt, Lv[v], u0), a * unn);
                 A.uout[v * vs + idx] = uo;
                 un[v] = uo;
@@ -947,17 +864,12 @@ size_t stage_smem_bytes(const Geo& g, int recon) {
     const size_t ring = g.ndim == 3 ? slots * NV * (pad ? cw * ch : P) : 0;
     const size_t cur = pad ? 0 : NV * cw * ch;
     const bool k16 = fast_shape(g);
-#ifdef EXP_NOFC
-    const size_t nst = 2;
-#else
     const size_t nst = k16 && policy_face_centric(g.ndim, recon, 16, 16) ? 1 : 2;  // FC: fluxes only
-#endif
     const size_t fx = nst * NV * (size_t)(nb0 + 1) * nb1;
     const size_t fy = g.ndim >= 2 ? nst * NV * (size_t)nb0 * (nb1 + 1) : 0;
-    const size_t stg = k16 && policy_stage_ops(g.ndim, recon, 16, 16) ? 2 * NV * P : 0;
     const size_t nh = 2 * (size_t)NG * (nb0 + nb1);
     const size_t hsm = k16 && g.ndim == 3 && nst == 1 ? NV * nh : 0;  // HSM staging
-    return (ring + cur + fx + fy + stg + hsm) * sizeof(double);
+    return (ring + cur + fx + fy + hsm) * sizeof(double);
 }
 
 cudaError_t launch_stage(const StageArgs& a, int recon, int riemann, cudaStream_t s) {
