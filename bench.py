@@ -177,6 +177,41 @@ def problem_for(args, world: int) -> si.Problem:
     return p
 
 
+# ------------------------------------------------------ secondary workload
+def secondary_run(name: str, steps: int, warmup: int, local: int) -> dict:
+    """The other scheme of BASELINE configs[3] (which does not name the
+    reconstruction): 256^3 Sedov, WENO5 + HLLC + SSP-RK3, timed the same way
+    (CUDA events on the library stream, after warm-up), one GPU."""
+    import torch
+
+    from paper_2401_03378_b200 import spark
+
+    q = si.PRESETS[name]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        s = spark.Spark(q.config(), device=local, stream=st)
+        s.set_primitive(si.sedov_device(q, device=f"cuda:{local}"))
+    for _ in range(warmup):
+        s.step()
+    st.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        s.step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    s.close()
+    zu = q.ncells * q.rk_stages * steps
+    bytes_step = sum(algorithmic_bytes_per_zone(q, k) for k in range(1, q.rk_stages + 1)) * q.ncells
+    peaks, kind = measured_peaks()
+    gbs = bytes_step * steps / (ms * 1e-3) / 1e9
+    return {"workload": name, "value": zu / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+            "warmup": warmup, "recon": "weno5", "rk_stages": q.rk_stages,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs / peaks["hbm_gbs"], "note": "whole step (FP64-bound scheme, DESIGN.md §4.3)"}}
+
+
 # ------------------------------------------------------------- N3 (AMR) leg
 def run_amr(args, rank: int, world: int, local: int) -> int:
     """NEXT N3 measurement: composite SSP-RK steps of the static two-level
@@ -246,25 +281,81 @@ def run_amr(args, rank: int, world: int, local: int) -> int:
 
 
 # ---------------------------------------------------------------- oracle leg
+def host_info() -> dict:
+    """CPU model and the oracle's compiler / flags."""
+    import subprocess
+
+    import oracle
+
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        cc = subprocess.check_output(["gcc", "--version"], text=True).splitlines()[0]
+    except Exception:  # pragma: no cover
+        cc = "gcc"
+    return {"cpu_model": model, "compiler": cc, "flags": " ".join(oracle.CFLAGS)}
+
+
 def oracle_sample(p: si.Problem, budget_s: float, max_steps: int = 1000):
     """Time the oracle (as it stands) on a bounded sample of the workload:
-    the same scheme / block shape on a 4x4x4-block (64^3) sub-grid of Sedov."""
+    the same scheme / block shape on a 4x4x4-block (64^3) sub-grid of Sedov,
+    on all host cores and on one; returns the rates, the sample state and the
+    step count (for the parity check of the GPU on the same sample)."""
     import oracle
 
     q = p.with_(nblk=tuple(min(4, p.nblk[d]) for d in range(3)))
-    U = oracle.prim_to_cons(q.ndim, q.gamma, si.initial_primitive(q))
-    U, _ = oracle.step(q.config(), U)  # warm-up (page-in, thread pool)
-    t0 = time.perf_counter()
-    steps = 0
-    while steps < max_steps:
-        U, _ = oracle.step(q.config(), U)
-        steps += 1
-        if time.perf_counter() - t0 >= budget_s:
-            break
-    el = time.perf_counter() - t0
-    zu = q.ncells * q.rk_stages * steps
-    return zu / el, oracle.num_threads(), f"{q.nb[0]}^3 blocks x {q.nblk[0]}x{q.nblk[1]}x{q.nblk[2]} " \
-        f"({q.ncells} cells, {q.name} scheme, Sedov), {steps} steps, {el:.1f} s"
+    U0 = oracle.prim_to_cons(q.ndim, q.gamma, si.initial_primitive(q))
+
+    def timed(budget, cap):
+        U, _ = oracle.step(q.config(), U0)  # warm-up (page-in, thread pool)
+        n = 1
+        t0 = time.perf_counter()
+        while n < cap:
+            U, _ = oracle.step(q.config(), U)
+            n += 1
+            if time.perf_counter() - t0 >= budget:
+                break
+        el = time.perf_counter() - t0
+        return q.ncells * q.rk_stages * (n - 1) / el, U, n, el
+
+    v_all, U, n, el = timed(budget_s, max_steps)
+    cores = oracle.num_threads()
+    oracle.set_threads(1)
+    try:
+        v_one = timed(budget_s / 3.0, max_steps)[0]
+    finally:
+        oracle.set_threads(0)
+    sample = (f"{q.nb[0]}^3 blocks x {q.nblk[0]}x{q.nblk[1]}x{q.nblk[2]} ({q.ncells} cells, {q.name} scheme, "
+              f"Sedov), {n - 1} timed steps, {el:.1f} s")
+    return v_all, cores, sample, v_one, q, U0, U, n
+
+
+def gpu_parity_on_sample(q: si.Problem, U0, Uo, nsteps: int) -> list:
+    """Per conserved variable, the GPU's error against the oracle after the
+    same nsteps CFL steps of the sample: max |g - o| / max|o_v| and the max
+    relative error where |o| > 1e-12 max|o_v| (reading R15)."""
+    from paper_2401_03378_b200 import spark
+
+    s = spark.Spark(q.config())
+    s.set_state(np.ascontiguousarray(U0))
+    for _ in range(nsteps):
+        s.step()
+    g = s.get_state().cpu().numpy()
+    s.close()
+    out = []
+    for v in range(Uo.shape[0]):
+        scale = float(np.max(np.abs(Uo[v])))
+        err = np.abs(g[v] - Uo[v])
+        big = np.abs(Uo[v]) > 1e-12 * scale
+        out.append({"var": v, "max_err_over_maxabs": float(err.max() / scale) if scale > 0 else float(err.max()),
+                    "max_rel_err": float(np.max(err[big] / np.abs(Uo[v][big]))) if big.any() else 0.0})
+    return out
 
 
 def run_reference(args, rank, world):
@@ -285,13 +376,14 @@ def run_reference(args, rank, world):
     zu = q.ncells * q.rk_stages * args.steps
     v = zu / el
     sample = f"{q.ncells}-cell sub-grid ({q.nblk[0]}x{q.nblk[1]}x{q.nblk[2]} blocks of 16^3) of {p.name}"
+    info = host_info()
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": p.name, "cells": p.ncells, "sampled_cells": q.ncells, "rk_stages": p.rk_stages},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, **info},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -326,6 +418,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-calibration", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the WENO5/RK3 line of configs[3] added to the default run")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -582,10 +676,17 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, sample = oracle_sample(p, args.cpu_budget)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        v, cores, sample, v_one, q, U0s, Uos, nst = oracle_sample(p, args.cpu_budget)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+               "single_thread": {"value": v_one, "unit": UNIT, "cores": 1}, **host_info(),
+               "parity_vs_gpu": {"steps": nst, "tolerance": "R15: 1e-12 |o| + 1e-15 max|o_v|",
+                                 "vars": gpu_parity_on_sample(q, U0s, Uos, nst)}}
 
     clocks = clk.summary()
+    secondary = None
+    if rank == 0 and world == 1 and args.config == "c4_sedov3d_plm" and not args.no_secondary and \
+            not (args.recon or args.riemann or args.grav or args.telescoping or args.graphs):
+        secondary = secondary_run("c4_sedov3d_weno", 10, 3, local)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -602,6 +703,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": total_launches,
             "clocks": clocks,
+            "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     s.close()

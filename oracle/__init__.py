@@ -101,6 +101,7 @@ def lib():
             "oracle_step_telescoping": (i32, [P(_Cfg), dp, d, d, d, dp]),
             "oracle_run": (i32, [P(_Cfg), dp, d, i64, dp, P(ctypes.c_long)]),
             "oracle_num_threads": (i32, []),
+            "oracle_set_threads": (None, [i32]),
             "oracle_amr_check": (i32, [P(_Amr)]),
             "oracle_amr_leaves": (i32, [P(_Amr), P(ctypes.c_long), P(ctypes.c_long)]),
             "oracle_amr_fill": (i32, [P(_Amr), dp, dp]),
@@ -351,6 +352,11 @@ def run(cfg, U, t_end=0.0, max_steps=0, t0=0.0):
 
 def num_threads() -> int:
     return lib().oracle_num_threads()
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle (n <= 0: all cores)."""
+    lib().oracle_set_threads(int(n))
 
 
 # ------------------------------------------------ NEXT N3: static two-level AMR

@@ -689,6 +689,18 @@ int oracle_run(const ocfg* c, double* U, double t_end, long max_steps, double* t
     return st;
 }
 
+/* Threads of the OpenMP loops (bench.py times the oracle on all host cores
+ * and on one); n <= 0 restores the default. */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    extern int omp_get_num_procs(void);
+    omp_set_num_threads(n > 0 ? n : omp_get_num_procs());
+#else
+    (void)n;
+#endif
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
     extern int omp_get_max_threads(void);

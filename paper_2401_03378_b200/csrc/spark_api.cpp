@@ -8,6 +8,7 @@
 // send/recv over NVLink, or device copies between virtual ranks) and the dt
 // all-reduce (ncclMin on the ordered bits of the CFL minimum).
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <climits>
@@ -44,6 +45,13 @@ struct Error : std::runtime_error {
         if (r_ != ncclSuccess)                                                                          \
             throw Error(SPARK_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));            \
     } while (0)
+
+// NVTX ranges (host-side, around the enqueue of each phase; visible in
+// Nsight Systems / ncu --nvtx): step, stage s, halo exchange, dt all-reduce
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
 
 int stencil_ng(int recon) {
     if (recon == SPARK_RECON_WENO5 || recon == SPARK_RECON_WENO5Z) return 3;
@@ -379,6 +387,7 @@ void exchange_local(const std::vector<spark_ctx*>& m) {
 // sees the same `bad` and rolls back (or reports) together.
 static_assert(offsetof(spark::DevScalars, bad) == offsetof(spark::DevScalars, acc) + 8, "acc/bad pair");
 void allreduce_acc(spark_ctx* c) {
+    Nvtx r("dt all-reduce (CFL min + failure word)");
     if (c->comm)
         NC(ncclAllReduce(&c->sc->acc, &c->sc->acc, 2, ncclUint64, ncclMin, c->comm, c->stream));
 }
@@ -502,6 +511,7 @@ void sync_and_check(spark_ctx* c, bool rollback_on_error, int old_n) {
 }
 
 void do_step(spark_ctx* c, double dt) {
+    Nvtx step_range("spark step");
     // single context (1 rank or NCCL); the caller set t_end through do_begin
     const int S = c->cfg.rk_stages;
     int newn = c->n_idx;
@@ -510,10 +520,13 @@ void do_step(spark_ctx* c, double dt) {
         newn = stage_buffers(S, c->n_idx, s, &pi, &po);
         double a, b;
         rk_coeffs(S, s, &a, &b);
+        static const char* names[3] = {"stage 1", "stage 2", "stage 3"};
+        Nvtx stage_range(names[s - 1]);
         if (c->comm) {
             // pack on the compute stream; the NCCL exchange runs on the comm
             // stream while the interior blocks (no exchanged face) compute;
             // the rank-boundary blocks wait for the received slabs
+            Nvtx halo_range("halo exchange (pack + NCCL send/recv)");
             pack_all(c, c->U[pi]);
             CU(cudaEventRecord(c->ev_packed, c->stream));
             CU(cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
@@ -1031,7 +1044,10 @@ spark_status spark_step_group(spark_ctx* const* ctxs, int32_t n, double dt, doub
                 stage_buffers(S, c->n_idx, s, &pi, &po);
                 pack_all(c, c->U[pi]);
             }
-            exchange_local(m);
+            {
+                Nvtx r("halo exchange (virtual ranks)");
+                exchange_local(m);
+            }
             for (spark_ctx* c : m) {
                 int pi, po;
                 stage_buffers(S, c->n_idx, s, &pi, &po);
@@ -1265,8 +1281,12 @@ static void tile_step_one(spark_ctx* ctx, double dt, double t_end) {
     if (!m.empty()) throw Error(SPARK_ERR_ARG, m);
     if (!ctx->tiles.ready) throw Error(SPARK_ERR_STATE, "telescoping tiles need spark_set_scratch first");
     launched(ctx, spark::launch_step_begin(ctx->sc, dt, t_end, ctx->cfg.cfl, ctx->stream), "step begin");
-    tile_pack(ctx);
-    if (ctx->comm) tile_exchange_nccl(ctx);
+    {
+        Nvtx r("telescoping shell exchange");
+        tile_pack(ctx);
+        if (ctx->comm) tile_exchange_nccl(ctx);
+    }
+    Nvtx r2("telescoping stages");
     tile_stages(ctx);
     allreduce_acc(ctx);
     ctx->n_idx = (ctx->n_idx + 1) % 3;
@@ -1294,7 +1314,10 @@ extern "C" spark_status spark_step_group_telescoping(spark_ctx* const* ctxs, int
             launched(m[r], spark::launch_step_begin(m[r]->sc, dt, t_end, m[r]->cfg.cfl, m[r]->stream), "step begin");
             tile_pack(m[r]);
         }
-        tile_exchange_local(m);  // the one exchange of the step
+        {
+            Nvtx r("telescoping shell exchange");
+            tile_exchange_local(m);  // the one exchange of the step
+        }
         for (spark_ctx* c : m) tile_stages(c);
         group_min(m);
         for (spark_ctx* c : m) c->n_idx = (c->n_idx + 1) % 3;

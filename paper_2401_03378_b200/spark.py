@@ -377,12 +377,24 @@ class Spark:
         return out
 
     def stage_apply(self, U_prev, U_n, a: float, b: float, dt: float, out=None):
+        """One fused stage on device tensors (canonical layout); synchronises
+        the library stream before returning, so `out` is ready to read."""
         torch = self.torch
         if out is None:
             out = torch.empty_like(U_prev)
+        for name, x in (("U_prev", U_prev), ("U_n", U_n), ("out", out)):
+            if x is None and name == "U_n":
+                if a != 0.0:
+                    raise ValueError("U_n is required when a != 0")
+                continue
+            if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()
+                    and x.numel() == int(np.prod(self.shape))):
+                raise ValueError(f"{name} must be a contiguous float64 CUDA tensor of {int(np.prod(self.shape))} "
+                                 "elements")
         _check(lib().spark_stage_apply(self.ctx, ctypes.c_void_p(U_prev.data_ptr()),
                                        ctypes.c_void_p(U_n.data_ptr()) if U_n is not None else None,
                                        a, b, dt, ctypes.c_void_p(out.data_ptr())), self.ctx, "stage_apply")
+        self.sync()
         return out
 
     def time(self):
