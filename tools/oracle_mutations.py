@@ -104,7 +104,9 @@ def run(name: str, text: str, tmp: str) -> tuple[bool, str]:
     subprocess.check_call(["gcc", *oracle.CFLAGS, "-o", so, c, "-lm"])
     pins = [p for p in PINS if os.path.exists(os.path.join(ROOT, p))]
     env = dict(os.environ, SPARK_ORACLE_LIB=so)
-    r = subprocess.run([sys.executable, "-m", "pytest", *pins, "-q", "-rf", "-p", "no:cacheprovider", "-n", "4"],
+    # a mutation that makes a pin run away (e.g. a wrong CFL dt) fails by timeout
+    r = subprocess.run([sys.executable, "-m", "pytest", *pins, "-q", "-rf", "-p", "no:cacheprovider", "-n", "4",
+                        "--timeout", "120"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1800)
     failed = sorted({ln.split()[1].split("::")[-1].split("[")[0] for ln in r.stdout.splitlines()
                      if ln.startswith("FAILED")})
