@@ -268,6 +268,17 @@ spark_status spark_step_telescoping(spark_ctx* ctx, double dt, double t_end, dou
  * U, the primitive tile, the face fluxes and the 2 x 26 shell buffers). */
 spark_status spark_telescoping_scratch_bytes(const spark_config* cfg, int32_t rank, int32_t nranks, size_t* bytes);
 
+/* Host-only: the telescoping shell plan of `rank` — per direction
+ * dir = (c0+1) + 3(c1+1) + 9(c2+1) (c_d in {-1, 0, 1}; 13 is the rank itself)
+ * the peer rank (-1: none) and the cells of the region (G = S*NGK along a
+ * nonzero component, the sub-box extent along a zero one; layout [v][z][y][x]
+ * of the region), and the posting order of the grouped exchange: ops[i] > 0
+ * receive direction ops[i]-1 from its peer, < 0 send the own region on side
+ * -ops[i]-1 to that direction's peer (receives ordered by the receiver's
+ * direction, sends by 26 - direction). */
+spark_status spark_telescoping_plan(const spark_config* cfg, int32_t rank, int32_t nranks, int32_t peer[27],
+                                    int64_t cells[27], int32_t ops[54], int32_t* nops);
+
 /* Give the context a caller-owned scratch (device, 256-byte aligned, >= the
  * bytes above) for the HBM telescoping path; selects that path for every
  * spark_step_telescoping of this context. */

@@ -642,18 +642,26 @@ void tile_pack(spark_ctx* c) {
 // sides order the messages between a pair of ranks by the receiver's
 // direction: my receives by my direction D, my sends by 26 - D (the peer
 // stores what I send for D as its direction 26 - D).
+// posting order of the shell messages: (is_send, direction)
+std::vector<std::pair<bool, int>> tile_ops(const int* peer) {
+    std::vector<std::pair<bool, int>> ops;
+    for (int k = 0; k < 27; k++) {
+        const int rd = k, sd = 26 - k;
+        if (peer[rd] >= 0) ops.emplace_back(false, rd);
+        if (peer[sd] >= 0) ops.emplace_back(true, sd);
+    }
+    return ops;
+}
+
 void tile_exchange_nccl(spark_ctx* c) {
     auto& T = c->tiles;
     const spark::Geo& g = c->plan.geo;
     NC(ncclGroupStart());
-    for (int k = 0; k < 27; k++) {
-        const int rd = k, sd = 26 - k;
-        if (T.peer[rd] >= 0)
-            NC(ncclRecv(T.recv[rd], (size_t)g.nvar * spark::tile_region_cells(T.tg, rd), ncclFloat64, T.peer[rd],
-                        c->comm, c->stream));
-        if (T.peer[sd] >= 0)
-            NC(ncclSend(T.send[sd], (size_t)g.nvar * spark::tile_region_cells(T.tg, sd), ncclFloat64, T.peer[sd],
-                        c->comm, c->stream));
+    for (const auto& op : tile_ops(T.peer)) {
+        const int dir = op.second;
+        const size_t n = (size_t)g.nvar * spark::tile_region_cells(T.tg, dir);
+        if (op.first) NC(ncclSend(T.send[dir], n, ncclFloat64, T.peer[dir], c->comm, c->stream));
+        else NC(ncclRecv(T.recv[dir], n, ncclFloat64, T.peer[dir], c->comm, c->stream));
     }
     NC(ncclGroupEnd());
 }
@@ -1267,6 +1275,25 @@ extern "C" spark_status spark_telescoping_scratch_bytes(const spark_config* cfg,
         if (!bytes) throw Error(SPARK_ERR_ARG, "null bytes");
         Plan p = make_plan(cfg, rank, nranks, nranks == 1);
         *bytes = tile_scratch_bytes(cfg, p);
+    });
+}
+
+extern "C" spark_status spark_telescoping_plan(const spark_config* cfg, int32_t rank, int32_t nranks,
+                                              int32_t peer[27], int64_t cells[27], int32_t ops[54],
+                                              int32_t* nops) {
+    return guard(nullptr, [&] {
+        if (!peer || !cells || !ops || !nops) throw Error(SPARK_ERR_ARG, "null output");
+        Plan p = make_plan(cfg, rank, nranks);
+        const spark::TileGeo t = tile_geo(cfg, p);
+        int pr[27];
+        for (int dir = 0; dir < 27; dir++) {
+            pr[dir] = dir == 13 ? -1 : tile_peer(p, dir);
+            peer[dir] = pr[dir];
+            cells[dir] = pr[dir] >= 0 ? spark::tile_region_cells(t, dir) : 0;
+        }
+        const auto o = tile_ops(pr);
+        *nops = (int32_t)o.size();
+        for (size_t i = 0; i < o.size(); i++) ops[i] = o[i].first ? -(o[i].second + 1) : o[i].second + 1;
     });
 }
 

@@ -27,6 +27,7 @@ EXPORTS = [
     "spark_step_group", "spark_stage_apply", "spark_profile_enable", "spark_profile_read",
     "spark_selftest_riemann", "spark_axpy", "spark_step_telescoping", "spark_run", "spark_set_time",
     "spark_step_host", "spark_telescoping_scratch_bytes", "spark_set_scratch", "spark_step_group_telescoping",
+    "spark_telescoping_plan",
     "spark_amr_leaves", "spark_amr_required_bytes", "spark_amr_init", "spark_amr_finalize", "spark_amr_last_error",
     "spark_amr_set_state", "spark_amr_get_state", "spark_amr_fill_guardcells", "spark_amr_step", "spark_amr_get_time",
 ]
@@ -128,6 +129,7 @@ def lib() -> ctypes.CDLL:
         "spark_step_host": (i32, [vp, vp, vp, d, d, i32]),
         "spark_telescoping_scratch_bytes": (i32, [cp, i32, i32, P(ctypes.c_size_t)]),
         "spark_set_scratch": (i32, [vp, vp, ctypes.c_size_t]),
+        "spark_telescoping_plan": (i32, [cp, i32, i32, P(i32), P(i64), P(i32), P(i32)]),
         "spark_step_group_telescoping": (i32, [P(vp), i32, d, d, P(d)]),
         "spark_amr_leaves": (i32, [cp, P(CRefine), P(i64), P(i64)]),
         "spark_amr_required_bytes": (i32, [cp, P(CRefine), P(ctypes.c_size_t)]),
@@ -170,6 +172,19 @@ def _check(st: int, ctx=None, what: str = ""):
 
 
 # ------------------------------------------------------------ host-only queries
+def telescoping_plan(cfg: dict, rank: int, nranks: int):
+    """(peer[27], cells[27], ops) of the telescoping shell exchange (host only);
+    ops: ("recv" | "send", direction) in posting order."""
+    c = to_cconfig(cfg)
+    peer = (ctypes.c_int32 * 27)()
+    cells = (ctypes.c_int64 * 27)()
+    ops = (ctypes.c_int32 * 54)()
+    n = ctypes.c_int32()
+    _check(lib().spark_telescoping_plan(ctypes.byref(c), rank, nranks, peer, cells, ops, ctypes.byref(n)),
+           what="telescoping_plan")
+    return list(peer), list(cells), [("recv", o - 1) if o > 0 else ("send", -o - 1) for o in ops[:n.value]]
+
+
 def check_config(cfg: dict, nranks: int = 1) -> bool:
     c = to_cconfig(cfg)
     return lib().spark_check_config(ctypes.byref(c), nranks) == SPARK_OK
