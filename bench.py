@@ -540,7 +540,9 @@ def main():
         ach = fp64_per_zone * zu_rate_kernel
         roofline_fp64 = {"bound": "alu", "achieved": ach / 1e12, "peak": fp64_peak / 1e12,
                          "unit": "T FP64 instr/s", "frac": ach / fp64_peak,
-                         "per_zone": fp64_per_zone, "source": "ncu instruction counts x live kernel time"}
+                         "per_zone": fp64_per_zone, "source": "ncu instruction counts x live kernel time",
+                         "peak_source": "builder-measured DFMA issue rate (tools/fp64_peak.cu -> "
+                                        "profiles/fp64_peak.json); MEASURED_PEAKS.json has no FP64 entry"}
 
     # issue view: executed warp instructions per zone-update (ncu) x the kernel's
     # zone rate, against the SM issue peak (4 schedulers x 1 warp-instr/clk x 148

@@ -358,7 +358,8 @@ spark_status spark_selftest_riemann(int32_t device, int32_t riemann, int32_t ndi
  * over the stages (fluxBuff, B <- b_s (B + F)); after the last stage the
  * coarse cells on a coarse-fine face take the mean of the fine fluxes
  * (communicate_fluxes + correction), which makes the step conservative.
- * Single GPU; nb even along refined dims; no gravity.  Errors as spark_step. */
+ * One rank, or virtual ranks on one device (below); nb even along refined
+ * dims; no gravity.  Errors as spark_step. */
 typedef struct {
     int32_t rlo[3], rhi[3];  /* refined coarse blocks [rlo, rhi); rlo == rhi: none */
 } spark_refine;
@@ -366,10 +367,28 @@ typedef struct {
 typedef struct spark_amr spark_amr;
 
 spark_status spark_amr_leaves(const spark_config* cfg, const spark_refine* ref, int64_t* ncoarse, int64_t* nfine);
+/* Leaves of `rank` when the leaf list is split into nranks contiguous ranges
+ * (Paramesh-style distribution of the ordered leaf list): first, count. */
+spark_status spark_amr_rank_leaves(const spark_config* cfg, const spark_refine* ref, int32_t rank, int32_t nranks,
+                                   int64_t* first, int64_t* count);
 spark_status spark_amr_required_bytes(const spark_config* cfg, const spark_refine* ref, size_t* bytes);
 /* arena: device memory of >= required bytes (256-byte aligned), caller-owned. */
 spark_status spark_amr_init(const spark_config* cfg, const spark_refine* ref, int32_t device, void* cuda_stream,
                             void* arena, size_t arena_bytes, spark_amr** out);
+/* Virtual ranks on one device (testing the multi-rank path): nranks members,
+ * each owning its range of leaves (spark_amr_rank_leaves) with its own state
+ * U[v][local leaf][cells] in arenas[r] (>= spark_amr_group_required_bytes).
+ * Per stage the guard values a member needs from another member's leaves are
+ * packed by their owner (copy or restriction) and copied over; per step the
+ * fine-face fluxBuff values a coarse cell's correction needs likewise
+ * (communicate_fluxes).  The result is bitwise that of one rank. */
+spark_status spark_amr_group_required_bytes(const spark_config* cfg, const spark_refine* ref, int32_t nranks,
+                                            size_t* bytes);
+spark_status spark_amr_init_local_group(const spark_config* cfg, const spark_refine* ref, int32_t nranks,
+                                        int32_t device, void* cuda_stream, void* const* arenas, size_t arena_bytes,
+                                        spark_amr** outs);
+/* One composite step of all members of a local group (failure: all or none roll back). */
+spark_status spark_amr_step_group(spark_amr* const* amrs, int32_t n, double dt, double t_end, double* dt_used);
 spark_status spark_amr_finalize(spark_amr* amr);
 const char* spark_amr_last_error(const spark_amr* amr);
 /* Load U[v][leaf][cells] (host or device); resets t and the step count. */

@@ -54,15 +54,15 @@ struct AmrGeo {
 
 struct GuardE {
     long long dst;  // leaf * np + padded index
-    long long src;  // leaf * nc + cell (first child for a restriction)
-    int kind;       // 1 copy, 2 restriction; bits 4+d: negate momentum d (reflect)
+    long long src;  // leaf * nc + cell (first child for a restriction); kind 3: slot of the received guards
+    int kind;       // 1 copy, 2 restriction, 3 received from another rank; bits 4+d: negate momentum d (reflect)
     int pad;
 };
 
 struct CorrE {
     long long cell;   // coarse leaf * nc + cell
     long long bc;     // (leaf * 6 + slot) * mf + face cell of the coarse side
-    long long bf[4];  // the fine faces (same encoding), 2^(ndim-1) of them
+    long long bf[4];  // the fine faces (same encoding), 2^(ndim-1) of them; -(slot+1): received from another rank
     int side;         // 1: interface on the coarse cell's high face
     int pad;
 };
@@ -95,11 +95,23 @@ __global__ void amr_interior_kernel(const AmrGeo g, const double* __restrict__ u
     if (!ok) flag_nonphysical(sc);
 }
 
+// conserved value v of a guard source: copy, or the restriction mean of the
+// 2^ndim fine children (diagonal pairs, reading R22)
+template <int NV>
+__device__ __forceinline__ double guard_value(const AmrGeo& g, const double* __restrict__ s, int kind) {
+    const long long ox = 1, oy = g.nb[0], oz = (long long)g.nb[0] * g.nb[1];
+    if (kind == 1) return s[0];
+    if (NV == 3) return (s[0] + s[ox]) * 0.5;
+    if (NV == 4) return ((s[0] + s[ox + oy]) + (s[ox] + s[oy])) * 0.25;
+    return (((s[0] + s[ox + oy]) + (s[ox] + s[oy])) + ((s[oz] + s[oz + ox + oy]) + (s[oz + ox] + s[oz + oy]))) *
+           0.125;
+}
+
 template <int NV>
 __global__ void amr_guard_kernel(const AmrGeo g, const double* __restrict__ u, const GuardE* __restrict__ ge,
-                                 long long n, double* __restrict__ w, int to_prim, DevScalars* sc) {
+                                 long long n, const double* __restrict__ grecv, double* __restrict__ w, int to_prim,
+                                 DevScalars* sc) {
     const long long vs = g.nleaf * g.nc, vp = g.nleaf * g.np;
-    const long long ox = 1, oy = g.nb[0], oz = (long long)g.nb[0] * g.nb[1];
     bool ok = true;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
          e += (long long)gridDim.x * blockDim.x) {
@@ -107,18 +119,7 @@ __global__ void amr_guard_kernel(const AmrGeo g, const double* __restrict__ u, c
         double uu[NV], ww[NV];
 #pragma unroll
         for (int v = 0; v < NV; v++) {
-            const double* s = u + v * vs + E.src;
-            double val;
-            if ((E.kind & 15) == 1) {
-                val = s[0];
-            } else if (NV == 3) {  // restriction: diagonal-pairwise mean (reading R22)
-                val = (s[0] + s[ox]) * 0.5;
-            } else if (NV == 4) {
-                val = ((s[0] + s[ox + oy]) + (s[ox] + s[oy])) * 0.25;
-            } else {
-                val = (((s[0] + s[ox + oy]) + (s[ox] + s[oy])) +
-                       ((s[oz] + s[oz + ox + oy]) + (s[oz + ox] + s[oz + oy]))) * 0.125;
-            }
+            double val = (E.kind & 15) == 3 ? grecv[E.src * NV + v] : guard_value<NV>(g, u + v * vs + E.src, E.kind & 15);
             if (v >= 1 && v < NV - 1 && ((E.kind >> (3 + v)) & 1)) val = -val;
             uu[v] = val;
         }
@@ -275,8 +276,8 @@ __global__ void amr_update_kernel(const AmrGeo g, const double* __restrict__ F, 
 // ---------------------------------------------------------------- KD
 template <int NV>
 __global__ void amr_corr_kernel(const AmrGeo g, const CorrE* __restrict__ ce, long long n, int d,
-                                const double* __restrict__ B, double* __restrict__ u, const double* __restrict__ dtp,
-                                DevScalars* sc) {
+                                const double* __restrict__ B, const double* __restrict__ frecv, double* __restrict__ u,
+                                const double* __restrict__ dtp, DevScalars* sc) {
     const long long vs = g.nleaf * g.nc, bvs = g.nleaf * 6 * g.mf;
     const double dt = *dtp;
     bool ok = true;
@@ -287,10 +288,12 @@ __global__ void amr_corr_kernel(const AmrGeo g, const CorrE* __restrict__ ce, lo
 #pragma unroll
         for (int v = 0; v < NV; v++) {
             const double* bv = B + v * bvs;
+            // a fine face on this rank, or received from the rank that owns it
+            auto fb = [&](int k) { return E.bf[k] >= 0 ? bv[E.bf[k]] : frecv[(-E.bf[k] - 1) * NV + v]; };
             double m;
-            if (NV == 3) m = bv[E.bf[0]];
-            else if (NV == 4) m = (bv[E.bf[0]] + bv[E.bf[1]]) * 0.5;
-            else m = ((bv[E.bf[0]] + bv[E.bf[3]]) + (bv[E.bf[1]] + bv[E.bf[2]])) * 0.25;  // diagonal pairs
+            if (NV == 3) m = fb(0);
+            else if (NV == 4) m = (fb(0) + fb(1)) * 0.5;
+            else m = ((fb(0) + fb(3)) + (fb(1) + fb(2))) * 0.25;  // diagonal pairs
             const double corr = dt * (bv[E.bc] - m) * g.rdx[0][d];
             double* uq = u + v * vs + E.cell;
             const double val = E.side ? *uq + corr : *uq - corr;
@@ -300,6 +303,31 @@ __global__ void amr_corr_kernel(const AmrGeo g, const CorrE* __restrict__ ce, lo
         ok &= cons_to_prim<NV>(uu, ww, g.gamma - 1.0);
     }
     if (!ok) flag_nonphysical(sc);
+}
+
+// ------------------------------------------------ communicate (multi-rank)
+// guard values another rank needs: copy or restriction of own cells, [item][v]
+template <int NV>
+__global__ void amr_gpack_kernel(const AmrGeo g, const double* __restrict__ u, const GuardE* __restrict__ it,
+                                 long long n, double* __restrict__ out) {
+    const long long vs = g.nleaf * g.nc;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
+        const GuardE E = it[e];
+#pragma unroll
+        for (int v = 0; v < NV; v++) out[e * NV + v] = guard_value<NV>(g, u + v * vs + E.src, E.kind & 15);
+    }
+}
+
+// fine-face fluxBuff values another rank's correction needs (communicate_fluxes), [item][v]
+template <int NV>
+__global__ void amr_fpack_kernel(const AmrGeo g, const double* __restrict__ B, const long long* __restrict__ idx,
+                                 long long n, double* __restrict__ out) {
+    const long long bvs = g.nleaf * 6 * g.mf;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int v = 0; v < NV; v++) out[e * NV + v] = B[v * bvs + idx[e]];
 }
 
 // ---------------------------------------------------------------- KE
@@ -628,7 +656,113 @@ AmrPlan make_amr_plan(const spark_config* c, const spark_refine* r) {
 
 size_t al(size_t x) { return (x + 255) / 256 * 256; }
 
-size_t amr_bytes(const AmrPlan& p) {
+// One rank's share of the composite grid: a contiguous range of the leaf
+// list (coarse leaves first, as in the global order), its guard map and
+// correction lists in local indices, and what it exchanges with the other
+// ranks: guard values (per stage) and fine-face fluxBuff values (per step,
+// communicate_fluxes).  Items for one peer are ordered identically on both
+// sides (the order of the receiver's entries), exchange buffers are
+// [item][v], grouped by peer rank.
+struct RankPlan {
+    AmrGeo g{};
+    long long l0 = 0, nloc = 0;
+    std::vector<GuardE> guards;
+    std::vector<CorrE> corr[3];
+    std::vector<GuardE> gsend;                  // src (local) + kind of each value sent
+    std::vector<long long> gsend_off, grecv_off;  // per peer rank, size nranks + 1
+    std::vector<long long> fsend;               // local B index (variable 0) of each value sent
+    std::vector<long long> fsend_off, frecv_off;
+};
+
+std::vector<RankPlan> partition(const AmrPlan& P, int nranks) {
+    const AmrGeo& G = P.g;
+    const long long L = G.nleaf;
+    if (nranks < 1 || nranks > L) throw AmrError(SPARK_ERR_ARG, "nranks must be 1..number of leaves");
+    std::vector<long long> l0(nranks + 1);
+    for (int r = 0; r <= nranks; r++) l0[r] = L * r / nranks;
+    auto owner = [&](long long leaf) {
+        int r = (int)(leaf * nranks / L);
+        while (leaf < l0[r]) r--;
+        while (leaf >= l0[r + 1]) r++;
+        return r;
+    };
+    std::vector<RankPlan> R(nranks);
+    // requests: greq[r][q] = entries of r reading a guard value owned by q
+    std::vector<std::vector<std::vector<std::pair<size_t, GuardE>>>> greq(nranks,
+        std::vector<std::vector<std::pair<size_t, GuardE>>>(nranks));
+    struct FReq { int d; size_t e; int k; long long qidx; };
+    std::vector<std::vector<std::vector<FReq>>> freq(nranks, std::vector<std::vector<FReq>>(nranks));
+    for (int r = 0; r < nranks; r++) {
+        RankPlan& rp = R[r];
+        rp.l0 = l0[r];
+        rp.nloc = l0[r + 1] - l0[r];
+        rp.g = G;
+        rp.g.nleaf = rp.nloc;
+        rp.g.ncl = std::max(0LL, std::min(G.ncl - rp.l0, rp.nloc));
+    }
+    for (const GuardE& E : P.guards) {
+        const long long leaf = E.dst / G.np;
+        const int r = owner(leaf);
+        GuardE e = E;
+        e.dst = (leaf - l0[r]) * G.np + (E.dst - leaf * G.np);
+        const long long sleaf = E.src / G.nc;
+        const int q = owner(sleaf);
+        if (q == r) {
+            e.src = E.src - l0[r] * G.nc;
+        } else {
+            GuardE item{};
+            item.src = E.src - l0[q] * G.nc;
+            item.kind = E.kind & 15;
+            greq[r][q].emplace_back(R[r].guards.size(), item);
+            e.kind = 3 | (E.kind & ~15);
+        }
+        R[r].guards.push_back(e);
+    }
+    const long long bstride = 6 * G.mf;
+    for (int d = 0; d < 3; d++)
+        for (const CorrE& E : P.corr[d]) {
+            const long long leaf = E.cell / G.nc;
+            const int r = owner(leaf);
+            CorrE e = E;
+            e.cell = E.cell - l0[r] * G.nc;
+            e.bc = E.bc - l0[r] * bstride;
+            const int nf = 1 << (G.ndim - 1);
+            for (int k = 0; k < nf; k++) {
+                const long long fleaf = E.bf[k] / bstride;
+                const int q = owner(fleaf);
+                if (q == r) e.bf[k] = E.bf[k] - l0[r] * bstride;
+                else freq[r][q].push_back({d, R[r].corr[d].size(), k, E.bf[k] - l0[q] * bstride});
+            }
+            R[r].corr[d].push_back(e);
+        }
+    // slots and send lists
+    for (int r = 0; r < nranks; r++) {
+        R[r].grecv_off.assign(nranks + 1, 0);
+        R[r].frecv_off.assign(nranks + 1, 0);
+        for (int q = 0; q < nranks; q++) {
+            R[r].grecv_off[q + 1] = R[r].grecv_off[q] + (long long)greq[r][q].size();
+            R[r].frecv_off[q + 1] = R[r].frecv_off[q] + (long long)freq[r][q].size();
+            for (size_t i = 0; i < greq[r][q].size(); i++) R[r].guards[greq[r][q][i].first].src = R[r].grecv_off[q] + i;
+            for (size_t i = 0; i < freq[r][q].size(); i++) {
+                const FReq& f = freq[r][q][i];
+                R[r].corr[f.d][f.e].bf[f.k] = -(R[r].frecv_off[q] + (long long)i + 1);
+            }
+        }
+    }
+    for (int q = 0; q < nranks; q++) {
+        R[q].gsend_off.assign(nranks + 1, 0);
+        R[q].fsend_off.assign(nranks + 1, 0);
+        for (int r = 0; r < nranks; r++) {
+            for (const auto& it : greq[r][q]) R[q].gsend.push_back(it.second);
+            for (const auto& f : freq[r][q]) R[q].fsend.push_back(f.qidx);
+            R[q].gsend_off[r + 1] = (long long)R[q].gsend.size();
+            R[q].fsend_off[r + 1] = (long long)R[q].fsend.size();
+        }
+    }
+    return R;
+}
+
+size_t rank_bytes(const RankPlan& p) {
     const AmrGeo& g = p.g;
     size_t b = al(sizeof(spark::DevScalars));
     b += 3 * al(sizeof(double) * g.nv * g.nleaf * g.nc);       // U^n and two stage buffers
@@ -637,13 +771,21 @@ size_t amr_bytes(const AmrPlan& p) {
     b += al(sizeof(double) * g.nv * g.nleaf * 6 * g.mf);        // fluxBuff
     b += al(sizeof(GuardE) * std::max<size_t>(1, p.guards.size()));
     for (int d = 0; d < 3; d++) b += al(sizeof(CorrE) * std::max<size_t>(1, p.corr[d].size()));
+    const size_t ngs = p.gsend.size(), ngr = p.grecv_off.empty() ? 0 : p.grecv_off.back();
+    const size_t nfs = p.fsend.size(), nfr = p.frecv_off.empty() ? 0 : p.frecv_off.back();
+    b += al(sizeof(GuardE) * std::max<size_t>(1, ngs)) + al(sizeof(long long) * std::max<size_t>(1, nfs));
+    b += al(sizeof(double) * g.nv * std::max<size_t>(1, ngs)) + al(sizeof(double) * g.nv * std::max<size_t>(1, ngr));
+    b += al(sizeof(double) * g.nv * std::max<size_t>(1, nfs)) + al(sizeof(double) * g.nv * std::max<size_t>(1, nfr));
     return b;
 }
 
 }  // namespace
 
 struct spark_amr {
-    AmrPlan plan;
+    AmrPlan plan;   // the global composite grid
+    RankPlan rp;    // this rank's share
+    int rank = 0, nranks = 1;
+    std::shared_ptr<std::vector<spark_amr*>> group;  // all members (itself when alone)
     int device = 0;
     cudaStream_t stream = nullptr;
     spark::DevScalars* sc = nullptr;
@@ -653,6 +795,9 @@ struct spark_amr {
     double* B = nullptr;
     GuardE* guards = nullptr;
     CorrE* corr[3] = {};
+    GuardE* gitems = nullptr;
+    long long* fitems = nullptr;
+    double *gsend = nullptr, *grecv = nullptr, *fsend = nullptr, *frecv = nullptr;
     int n_idx = 0;
     bool have_state = false;
     std::string err;
@@ -681,25 +826,25 @@ void launched(cudaError_t e, const char* what) {
 
 // padded tiles of state u: interior + face guards; primitives (to_prim) or conserved
 void amr_fill(spark_amr* a, const double* u, double* w, int to_prim) {
-    const AmrGeo& g = a->plan.g;
-    const long long nG = (long long)a->plan.guards.size();
+    const AmrGeo& g = a->rp.g;
+    const long long nG = (long long)a->rp.guards.size();
     const unsigned gi = spark::grid_of(g.nleaf * g.nc), gg = spark::grid_of(nG);
     if (g.ndim == 1) {
         spark::amr_interior_kernel<3><<<gi, 256, 0, a->stream>>>(g, u, w, to_prim, a->sc);
-        if (nG) spark::amr_guard_kernel<3><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, w, to_prim, a->sc);
+        if (nG) spark::amr_guard_kernel<3><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, a->grecv, w, to_prim, a->sc);
     } else if (g.ndim == 2) {
         spark::amr_interior_kernel<4><<<gi, 256, 0, a->stream>>>(g, u, w, to_prim, a->sc);
-        if (nG) spark::amr_guard_kernel<4><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, w, to_prim, a->sc);
+        if (nG) spark::amr_guard_kernel<4><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, a->grecv, w, to_prim, a->sc);
     } else {
         spark::amr_interior_kernel<5><<<gi, 256, 0, a->stream>>>(g, u, w, to_prim, a->sc);
-        if (nG) spark::amr_guard_kernel<5><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, w, to_prim, a->sc);
+        if (nG) spark::amr_guard_kernel<5><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, a->grecv, w, to_prim, a->sc);
     }
     launched(cudaGetLastError(), "amr fill");
 }
 
 template <int NDIM>
 void faces_d(spark_amr* a, double bco) {
-    const AmrGeo& g = a->plan.g;
+    const AmrGeo& g = a->rp.g;
     const unsigned gr = spark::grid_of(g.nleaf * g.NF);
     const int rs = a->plan.c.riemann;
     if (rs == 0) spark::amr_face_kernel<NDIM, 0><<<gr, 256, 0, a->stream>>>(g, a->W, a->F, a->B, bco);
@@ -709,7 +854,8 @@ void faces_d(spark_amr* a, double bco) {
 }
 
 void amr_stage(spark_amr* a, const double* prev, const double* un, double sa, double sb, double* out) {
-    const AmrGeo& g = a->plan.g;
+    const AmrGeo& g = a->rp.g;
+    if (g.nleaf == 0) return;
     amr_fill(a, prev, a->W, 1);
     if (g.ndim == 1) faces_d<1>(a, sb);
     else if (g.ndim == 2) faces_d<2>(a, sb);
@@ -722,7 +868,8 @@ void amr_stage(spark_amr* a, const double* prev, const double* un, double sa, do
 }
 
 void amr_cfl(spark_amr* a, const double* u) {
-    const AmrGeo& g = a->plan.g;
+    const AmrGeo& g = a->rp.g;
+    if (g.nleaf == 0) return;
     const unsigned gr = spark::grid_of(g.nleaf * g.nc);
     if (g.ndim == 1) spark::amr_cfl_kernel<1><<<gr, 256, 0, a->stream>>>(g, u, a->sc);
     else if (g.ndim == 2) spark::amr_cfl_kernel<2><<<gr, 256, 0, a->stream>>>(g, u, a->sc);
@@ -731,15 +878,56 @@ void amr_cfl(spark_amr* a, const double* u) {
 }
 
 void amr_correct(spark_amr* a, double* u) {
-    const AmrGeo& g = a->plan.g;
+    const AmrGeo& g = a->rp.g;
     for (int d = 0; d < g.ndim; d++) {  // one launch per direction: no two threads touch one cell
-        const long long n = (long long)a->plan.corr[d].size();
+        const long long n = (long long)a->rp.corr[d].size();
         if (!n) continue;
         const unsigned gr = spark::grid_of(n);
-        if (g.ndim == 1) spark::amr_corr_kernel<3><<<gr, 256, 0, a->stream>>>(g, a->corr[d], n, d, a->B, u, &a->sc->dt, a->sc);
-        else if (g.ndim == 2) spark::amr_corr_kernel<4><<<gr, 256, 0, a->stream>>>(g, a->corr[d], n, d, a->B, u, &a->sc->dt, a->sc);
-        else spark::amr_corr_kernel<5><<<gr, 256, 0, a->stream>>>(g, a->corr[d], n, d, a->B, u, &a->sc->dt, a->sc);
+        if (g.ndim == 1)
+            spark::amr_corr_kernel<3><<<gr, 256, 0, a->stream>>>(g, a->corr[d], n, d, a->B, a->frecv, u, &a->sc->dt, a->sc);
+        else if (g.ndim == 2)
+            spark::amr_corr_kernel<4><<<gr, 256, 0, a->stream>>>(g, a->corr[d], n, d, a->B, a->frecv, u, &a->sc->dt, a->sc);
+        else
+            spark::amr_corr_kernel<5><<<gr, 256, 0, a->stream>>>(g, a->corr[d], n, d, a->B, a->frecv, u, &a->sc->dt, a->sc);
         launched(cudaGetLastError(), "amr correction");
+    }
+}
+
+// the guard values (u: each member's U^(s-1)) or the fluxBuff values the other
+// ranks need: pack, then copy member q's slice for r into r's receive buffer
+void amr_exchange(const std::vector<spark_amr*>& m, const int* uidx, bool fluxes) {
+    if (m.size() < 2) return;
+    for (size_t r = 0; r < m.size(); r++) {
+        spark_amr* a = m[r];
+        const AmrGeo& g = a->rp.g;
+        const long long n = fluxes ? (long long)a->rp.fsend.size() : (long long)a->rp.gsend.size();
+        if (!n) continue;
+        const unsigned gr = spark::grid_of(n);
+        const double* u = uidx ? a->U[uidx[r]] : nullptr;
+        if (fluxes) {
+            if (g.nv == 3) spark::amr_fpack_kernel<3><<<gr, 256, 0, a->stream>>>(g, a->B, a->fitems, n, a->fsend);
+            else if (g.nv == 4) spark::amr_fpack_kernel<4><<<gr, 256, 0, a->stream>>>(g, a->B, a->fitems, n, a->fsend);
+            else spark::amr_fpack_kernel<5><<<gr, 256, 0, a->stream>>>(g, a->B, a->fitems, n, a->fsend);
+        } else {
+            if (g.nv == 3) spark::amr_gpack_kernel<3><<<gr, 256, 0, a->stream>>>(g, u, a->gitems, n, a->gsend);
+            else if (g.nv == 4) spark::amr_gpack_kernel<4><<<gr, 256, 0, a->stream>>>(g, u, a->gitems, n, a->gsend);
+            else spark::amr_gpack_kernel<5><<<gr, 256, 0, a->stream>>>(g, u, a->gitems, n, a->gsend);
+        }
+        launched(cudaGetLastError(), "amr pack");
+    }
+    for (size_t r = 0; r < m.size(); r++) {
+        spark_amr* a = m[r];
+        const int nv = a->rp.g.nv;
+        for (size_t q = 0; q < m.size(); q++) {
+            if (q == r) continue;
+            const auto& roff = fluxes ? a->rp.frecv_off : a->rp.grecv_off;
+            const auto& soff = fluxes ? m[q]->rp.fsend_off : m[q]->rp.gsend_off;
+            const long long n = roff[q + 1] - roff[q];
+            if (!n) continue;
+            double* dst = (fluxes ? a->frecv : a->grecv) + roff[q] * nv;
+            const double* src = (fluxes ? m[q]->fsend : m[q]->gsend) + soff[r] * nv;
+            ACU(cudaMemcpyAsync(dst, src, sizeof(double) * n * nv, cudaMemcpyDeviceToDevice, a->stream));
+        }
     }
 }
 
@@ -748,6 +936,116 @@ spark::DevScalars read_sc(spark_amr* a) {
     spark::DevScalars h;
     ACU(cudaMemcpy(&h, a->sc, sizeof(h), cudaMemcpyDeviceToHost));
     return h;
+}
+
+void carve_member(spark_amr* a, void* arena, size_t arena_bytes) {
+    const size_t need = rank_bytes(a->rp);
+    if (!arena) throw AmrError(SPARK_ERR_ARG, "null arena");
+    if (arena_bytes < need) throw AmrError(SPARK_ERR_OOM, "arena smaller than the required bytes");
+    if (reinterpret_cast<uintptr_t>(arena) % 256) throw AmrError(SPARK_ERR_ARG, "arena must be 256-byte aligned");
+    ACU(cudaSetDevice(a->device));
+    const AmrGeo& g = a->rp.g;
+    const RankPlan& rp = a->rp;
+    char* p = static_cast<char*>(arena);
+    auto take = [&](size_t bytes) {
+        char* q = p;
+        p += al(bytes);
+        return q;
+    };
+    a->sc = reinterpret_cast<spark::DevScalars*>(take(sizeof(spark::DevScalars)));
+    for (int i = 0; i < 3; i++) a->U[i] = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * g.nc));
+    a->W = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * g.np));
+    a->F = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * g.NF));
+    a->B = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * 6 * g.mf));
+    a->guards = reinterpret_cast<GuardE*>(take(sizeof(GuardE) * std::max<size_t>(1, rp.guards.size())));
+    for (int d = 0; d < 3; d++)
+        a->corr[d] = reinterpret_cast<CorrE*>(take(sizeof(CorrE) * std::max<size_t>(1, rp.corr[d].size())));
+    const size_t ngs = rp.gsend.size(), ngr = rp.grecv_off.back(), nfs = rp.fsend.size(), nfr = rp.frecv_off.back();
+    a->gitems = reinterpret_cast<GuardE*>(take(sizeof(GuardE) * std::max<size_t>(1, ngs)));
+    a->fitems = reinterpret_cast<long long*>(take(sizeof(long long) * std::max<size_t>(1, nfs)));
+    a->gsend = reinterpret_cast<double*>(take(sizeof(double) * g.nv * std::max<size_t>(1, ngs)));
+    a->grecv = reinterpret_cast<double*>(take(sizeof(double) * g.nv * std::max<size_t>(1, ngr)));
+    a->fsend = reinterpret_cast<double*>(take(sizeof(double) * g.nv * std::max<size_t>(1, nfs)));
+    a->frecv = reinterpret_cast<double*>(take(sizeof(double) * g.nv * std::max<size_t>(1, nfr)));
+    auto up = [&](void* dst, const void* src, size_t bytes) {
+        if (bytes) ACU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, a->stream));
+    };
+    up(a->guards, rp.guards.data(), sizeof(GuardE) * rp.guards.size());
+    for (int d = 0; d < 3; d++) up(a->corr[d], rp.corr[d].data(), sizeof(CorrE) * rp.corr[d].size());
+    up(a->gitems, rp.gsend.data(), sizeof(GuardE) * ngs);
+    up(a->fitems, rp.fsend.data(), sizeof(long long) * nfs);
+    launched(spark::launch_scalars_reset(a->sc, a->stream), "scalars reset");
+    ACU(cudaStreamSynchronize(a->stream));  // the host plan vectors are the copy sources
+}
+
+// one composite step of every member (a group of one: the single-rank path)
+void group_step(const std::vector<spark_amr*>& m, double dt, double t_end) {
+    spark_amr* a0 = m[0];
+    const int S = a0->plan.c.rk_stages;
+    auto group_min = [&]() {
+        if (m.size() < 2) return;
+        spark::AccPtrs p{};
+        for (size_t r = 0; r < m.size(); r++) p.p[r] = &m[r]->sc->acc;
+        launched(spark::launch_group_min(p, (int)m.size(), a0->stream), "group min");
+    };
+    group_min();  // the global CFL minimum of U^n (set_state computes it per member)
+    std::vector<int> n(m.size()), x(m.size()), y(m.size());
+    for (size_t r = 0; r < m.size(); r++) {
+        spark_amr* a = m[r];
+        if (!a->have_state) throw AmrError(SPARK_ERR_STATE, "no state loaded");
+        n[r] = a->n_idx, x[r] = (n[r] + 1) % 3, y[r] = (n[r] + 2) % 3;
+        launched(spark::launch_step_begin(a->sc, dt, t_end, a->plan.c.cfl, a->stream), "step begin");
+        const AmrGeo& g = a->rp.g;
+        ACU(cudaMemsetAsync(a->B, 0, sizeof(double) * g.nv * std::max(1LL, g.nleaf) * 6 * g.mf, a->stream));
+    }
+    // Shu-Osher stages: RK2 n->x, (x,n)->y; RK3 n->x, (x,n)->y, (y,n)->x
+    static const double ca[2][3] = {{0.0, 0.5, 0.0}, {0.0, 0.75, 1.0 / 3.0}};
+    static const double cb[2][3] = {{1.0, 0.5, 0.0}, {1.0, 0.25, 2.0 / 3.0}};
+    const int row = S == 2 ? 0 : 1;
+    for (int s = 0; s < S; s++) {
+        std::vector<int> pi(m.size()), po(m.size());
+        for (size_t r = 0; r < m.size(); r++) {
+            const int prev[3] = {n[r], x[r], y[r]}, outb[3] = {x[r], y[r], x[r]};
+            pi[r] = prev[s];
+            po[r] = outb[s];
+        }
+        amr_exchange(m, pi.data(), false);  // guard values across ranks (fill_guardcells)
+        for (size_t r = 0; r < m.size(); r++)
+            amr_stage(m[r], m[r]->U[pi[r]], m[r]->U[n[r]], ca[row][s], cb[row][s], m[r]->U[po[r]]);
+    }
+    amr_exchange(m, nullptr, true);  // communicate_fluxes
+    for (size_t r = 0; r < m.size(); r++) {
+        const int newn = S == 2 ? y[r] : x[r];
+        amr_correct(m[r], m[r]->U[newn]);  // flux correction
+        amr_cfl(m[r], m[r]->U[newn]);      // CFL minimum of the corrected state: dt of the next step
+        m[r]->n_idx = newn;
+    }
+    group_min();
+}
+
+// synchronise; on a failure roll back every member (the failing step) or none
+void group_check(const std::vector<spark_amr*>& m, const std::vector<int>& old, double* dt_used) {
+    std::vector<spark::DevScalars> h(m.size());
+    for (size_t r = 0; r < m.size(); r++) h[r] = read_sc(m[r]);
+    if (h[0].bad != spark::kNoBad) {
+        const bool now = h[0].active && h[0].bad == (unsigned long long)h[0].steps;
+        if (now) {
+            for (size_t r = 0; r < m.size(); r++) {
+                spark::DevScalars x = h[r];
+                m[r]->n_idx = old[r];
+                x.t = x.t_prev;
+                x.steps -= 1;
+                x.acc = x.acc_prev;
+                x.bad = spark::kNoBad;
+                x.status = 0;
+                ACU(cudaMemcpy(m[r]->sc, &x, sizeof(x), cudaMemcpyHostToDevice));
+            }
+            throw AmrError(SPARK_ERR_NONPHYSICAL, "non-physical state; rolled back to U^n");
+        }
+        throw AmrError(SPARK_ERR_NONPHYSICAL, "non-physical state in step " + std::to_string(h[0].bad) +
+                                                  "; later steps were frozen, state not rolled back");
+    }
+    if (dt_used) *dt_used = h[0].dt;
 }
 
 }  // namespace
@@ -762,63 +1060,75 @@ spark_status spark_amr_leaves(const spark_config* cfg, const spark_refine* ref, 
     });
 }
 
+spark_status spark_amr_rank_leaves(const spark_config* cfg, const spark_refine* ref, int32_t rank, int32_t nranks,
+                                   int64_t* first, int64_t* count) {
+    return amr_guard(nullptr, [&] {
+        AmrPlan p = make_amr_plan(cfg, ref);
+        if (nranks < 1 || nranks > p.g.nleaf || rank < 0 || rank >= nranks)
+            throw AmrError(SPARK_ERR_ARG, "bad rank / nranks");
+        const long long a = p.g.nleaf * rank / nranks, b = p.g.nleaf * (rank + 1) / nranks;
+        if (first) *first = a;
+        if (count) *count = b - a;
+    });
+}
+
 spark_status spark_amr_required_bytes(const spark_config* cfg, const spark_refine* ref, size_t* bytes) {
     return amr_guard(nullptr, [&] {
         if (!bytes) throw AmrError(SPARK_ERR_ARG, "null bytes");
-        *bytes = amr_bytes(make_amr_plan(cfg, ref));
+        *bytes = rank_bytes(partition(make_amr_plan(cfg, ref), 1)[0]);
+    });
+}
+
+spark_status spark_amr_group_required_bytes(const spark_config* cfg, const spark_refine* ref, int32_t nranks,
+                                            size_t* bytes) {
+    return amr_guard(nullptr, [&] {
+        if (!bytes) throw AmrError(SPARK_ERR_ARG, "null bytes");
+        size_t b = 0;
+        for (const RankPlan& rp : partition(make_amr_plan(cfg, ref), nranks)) b = std::max(b, rank_bytes(rp));
+        *bytes = b;
     });
 }
 
 spark_status spark_amr_init(const spark_config* cfg, const spark_refine* ref, int32_t device, void* cuda_stream,
                             void* arena, size_t arena_bytes, spark_amr** out) {
-    if (!out) return SPARK_ERR_ARG;
-    *out = nullptr;
-    std::unique_ptr<spark_amr> a(new spark_amr());
+    return spark_amr_init_local_group(cfg, ref, 1, device, cuda_stream, &arena, arena_bytes, out);
+}
+
+spark_status spark_amr_init_local_group(const spark_config* cfg, const spark_refine* ref, int32_t nranks,
+                                        int32_t device, void* cuda_stream, void* const* arenas, size_t arena_bytes,
+                                        spark_amr** outs) {
+    if (!outs || !arenas || nranks < 1 || nranks > spark::kMaxGroup) return SPARK_ERR_ARG;
+    std::vector<std::unique_ptr<spark_amr>> made;
     spark_status st = amr_guard(nullptr, [&] {
-        a->plan = make_amr_plan(cfg, ref);
-        a->device = device;
-        a->stream = static_cast<cudaStream_t>(cuda_stream);
-        const size_t need = amr_bytes(a->plan);
-        if (!arena) throw AmrError(SPARK_ERR_ARG, "null arena");
-        if (arena_bytes < need) throw AmrError(SPARK_ERR_OOM, "arena smaller than spark_amr_required_bytes");
-        if (reinterpret_cast<uintptr_t>(arena) % 256) throw AmrError(SPARK_ERR_ARG, "arena must be 256-byte aligned");
-        ACU(cudaSetDevice(device));
-        const AmrGeo& g = a->plan.g;
-        char* p = static_cast<char*>(arena);
-        a->sc = reinterpret_cast<spark::DevScalars*>(p);
-        p += al(sizeof(spark::DevScalars));
-        for (int i = 0; i < 3; i++) {
-            a->U[i] = reinterpret_cast<double*>(p);
-            p += al(sizeof(double) * g.nv * g.nleaf * g.nc);
+        AmrPlan P = make_amr_plan(cfg, ref);
+        std::vector<RankPlan> R = partition(P, nranks);
+        auto grp = std::make_shared<std::vector<spark_amr*>>();
+        for (int r = 0; r < nranks; r++) {
+            std::unique_ptr<spark_amr> a(new spark_amr());
+            a->plan = P;
+            a->rp = R[r];
+            a->rank = r;
+            a->nranks = nranks;
+            a->device = device;
+            a->stream = static_cast<cudaStream_t>(cuda_stream);
+            a->group = grp;
+            carve_member(a.get(), arenas[r], arena_bytes);
+            grp->push_back(a.get());
+            made.push_back(std::move(a));
         }
-        a->W = reinterpret_cast<double*>(p);
-        p += al(sizeof(double) * g.nv * g.nleaf * g.np);
-        a->F = reinterpret_cast<double*>(p);
-        p += al(sizeof(double) * g.nv * g.nleaf * g.NF);
-        a->B = reinterpret_cast<double*>(p);
-        p += al(sizeof(double) * g.nv * g.nleaf * 6 * g.mf);
-        a->guards = reinterpret_cast<GuardE*>(p);
-        p += al(sizeof(GuardE) * std::max<size_t>(1, a->plan.guards.size()));
-        if (!a->plan.guards.empty())
-            ACU(cudaMemcpyAsync(a->guards, a->plan.guards.data(), sizeof(GuardE) * a->plan.guards.size(),
-                                cudaMemcpyHostToDevice, a->stream));
-        for (int d = 0; d < 3; d++) {
-            a->corr[d] = reinterpret_cast<CorrE*>(p);
-            p += al(sizeof(CorrE) * std::max<size_t>(1, a->plan.corr[d].size()));
-            if (!a->plan.corr[d].empty())
-                ACU(cudaMemcpyAsync(a->corr[d], a->plan.corr[d].data(), sizeof(CorrE) * a->plan.corr[d].size(),
-                                    cudaMemcpyHostToDevice, a->stream));
-        }
-        launched(spark::launch_scalars_reset(a->sc, a->stream), "scalars reset");
-        ACU(cudaStreamSynchronize(a->stream));  // the host plan vectors are the copy sources
     });
-    if (st == SPARK_OK) *out = a.release();
-    return st;
+    if (st != SPARK_OK) return st;
+    for (int r = 0; r < nranks; r++) outs[r] = made[r].release();
+    return SPARK_OK;
 }
 
 spark_status spark_amr_finalize(spark_amr* a) {
     if (!a) return SPARK_ERR_ARG;
     spark_status st = amr_guard(a, [&] { ACU(cudaStreamSynchronize(a->stream)); });
+    if (a->group) {
+        auto& m = *a->group;
+        m.erase(std::remove(m.begin(), m.end(), a), m.end());
+    }
     delete a;
     return st;
 }
@@ -829,10 +1139,11 @@ spark_status spark_amr_set_state(spark_amr* a, const double* U, int32_t on_devic
     if (!a || !U) return SPARK_ERR_ARG;
     return amr_guard(a, [&] {
         ACU(cudaSetDevice(a->device));
-        const AmrGeo& g = a->plan.g;
+        const AmrGeo& g = a->rp.g;
         a->n_idx = 0;
-        ACU(cudaMemcpyAsync(a->U[0], U, sizeof(double) * g.nv * g.nleaf * g.nc,
-                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, a->stream));
+        if (g.nleaf)
+            ACU(cudaMemcpyAsync(a->U[0], U, sizeof(double) * g.nv * g.nleaf * g.nc,
+                                on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, a->stream));
         launched(spark::launch_scalars_reset(a->sc, a->stream), "scalars reset");
         amr_cfl(a, a->U[0]);
         a->have_state = true;
@@ -844,9 +1155,10 @@ spark_status spark_amr_get_state(spark_amr* a, double* U, int32_t on_device) {
     return amr_guard(a, [&] {
         if (!a->have_state) throw AmrError(SPARK_ERR_STATE, "no state loaded");
         ACU(cudaSetDevice(a->device));
-        const AmrGeo& g = a->plan.g;
-        ACU(cudaMemcpyAsync(U, a->U[a->n_idx], sizeof(double) * g.nv * g.nleaf * g.nc,
-                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, a->stream));
+        const AmrGeo& g = a->rp.g;
+        if (g.nleaf)
+            ACU(cudaMemcpyAsync(U, a->U[a->n_idx], sizeof(double) * g.nv * g.nleaf * g.nc,
+                                on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, a->stream));
         spark::DevScalars h = read_sc(a);
         if (h.bad != spark::kNoBad)
             throw AmrError(SPARK_ERR_NONPHYSICAL, "non-physical state in step " + std::to_string(h.bad));
@@ -857,8 +1169,9 @@ spark_status spark_amr_fill_guardcells(spark_amr* a, double* padded_out) {
     if (!a || !padded_out) return SPARK_ERR_ARG;
     return amr_guard(a, [&] {
         if (!a->have_state) throw AmrError(SPARK_ERR_STATE, "no state loaded");
+        if (a->nranks != 1) throw AmrError(SPARK_ERR_STATE, "spark_amr_fill_guardcells needs a single-rank context");
         ACU(cudaSetDevice(a->device));
-        const AmrGeo& g = a->plan.g;
+        const AmrGeo& g = a->rp.g;
         // corners / edges are never written: NaN, as in the oracle
         ACU(cudaMemsetAsync(padded_out, 0xff, sizeof(double) * g.nv * g.nleaf * g.np, a->stream));
         amr_fill(a, a->U[a->n_idx], padded_out, 0);
@@ -868,42 +1181,26 @@ spark_status spark_amr_fill_guardcells(spark_amr* a, double* padded_out) {
 spark_status spark_amr_step(spark_amr* a, double dt, double t_end, double* dt_used) {
     if (!a) return SPARK_ERR_ARG;
     return amr_guard(a, [&] {
-        if (!a->have_state) throw AmrError(SPARK_ERR_STATE, "no state loaded");
+        if (a->nranks != 1) throw AmrError(SPARK_ERR_STATE, "local-group contexts step with spark_amr_step_group");
         ACU(cudaSetDevice(a->device));
-        const AmrGeo& g = a->plan.g;
-        const int S = a->plan.c.rk_stages, n = a->n_idx;
-        const int x = (n + 1) % 3, y = (n + 2) % 3;
-        launched(spark::launch_step_begin(a->sc, dt, t_end, a->plan.c.cfl, a->stream), "step begin");
-        ACU(cudaMemsetAsync(a->B, 0, sizeof(double) * g.nv * g.nleaf * 6 * g.mf, a->stream));
-        // Shu-Osher stages: RK2 n->x, (x,n)->y; RK3 n->x, (x,n)->y, (y,n)->x
-        static const double ca[3][3] = {{0.0, 0.5, 0.0}, {0.0, 0.75, 1.0 / 3.0}, {0, 0, 0}};
-        static const double cb[3][3] = {{1.0, 0.5, 0.0}, {1.0, 0.25, 2.0 / 3.0}, {0, 0, 0}};
-        const int row = S == 2 ? 0 : 1;
-        const int prev[3] = {n, x, y}, outb[3] = {x, y, x};
-        for (int s = 0; s < S; s++)
-            amr_stage(a, a->U[prev[s]], a->U[n], ca[row][s], cb[row][s], a->U[outb[s]]);
-        const int newn = S == 2 ? y : x;
-        amr_correct(a, a->U[newn]);  // communicate_fluxes + flux correction
-        amr_cfl(a, a->U[newn]);      // CFL minimum of the corrected state: dt of the next step
-        a->n_idx = newn;
-        if (dt_used) {
-            spark::DevScalars h = read_sc(a);
-            if (h.bad != spark::kNoBad) {
-                if (h.active && h.bad == (unsigned long long)h.steps) {  // roll back this step
-                    a->n_idx = n;
-                    h.t = h.t_prev;
-                    h.steps -= 1;
-                    h.acc = h.acc_prev;
-                    h.bad = spark::kNoBad;
-                    h.status = 0;
-                    ACU(cudaMemcpy(a->sc, &h, sizeof(h), cudaMemcpyHostToDevice));
-                    throw AmrError(SPARK_ERR_NONPHYSICAL, "non-physical state; rolled back to U^n");
-                }
-                throw AmrError(SPARK_ERR_NONPHYSICAL, "non-physical state in step " + std::to_string(h.bad) +
-                                                          "; later steps were frozen, state not rolled back");
-            }
-            *dt_used = h.dt;
-        }
+        std::vector<spark_amr*> m{a};
+        std::vector<int> old{a->n_idx};
+        group_step(m, dt, t_end);
+        if (dt_used) group_check(m, old, dt_used);
+    });
+}
+
+spark_status spark_amr_step_group(spark_amr* const* amrs, int32_t n, double dt, double t_end, double* dt_used) {
+    if (!amrs || n < 1 || !amrs[0]) return SPARK_ERR_ARG;
+    spark_amr* a0 = amrs[0];
+    return amr_guard(a0, [&] {
+        if (!a0->group || (int)a0->group->size() != n) throw AmrError(SPARK_ERR_ARG, "needs all members of one group");
+        ACU(cudaSetDevice(a0->device));
+        std::vector<spark_amr*> m(*a0->group);
+        std::vector<int> old;
+        for (spark_amr* a : m) old.push_back(a->n_idx);
+        group_step(m, dt, t_end);
+        if (dt_used) group_check(m, old, dt_used);
     });
 }
 

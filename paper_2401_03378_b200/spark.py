@@ -30,6 +30,7 @@ EXPORTS = [
     "spark_telescoping_plan",
     "spark_amr_leaves", "spark_amr_required_bytes", "spark_amr_init", "spark_amr_finalize", "spark_amr_last_error",
     "spark_amr_set_state", "spark_amr_get_state", "spark_amr_fill_guardcells", "spark_amr_step", "spark_amr_get_time",
+    "spark_amr_rank_leaves", "spark_amr_group_required_bytes", "spark_amr_init_local_group", "spark_amr_step_group",
 ]
 
 
@@ -141,6 +142,10 @@ def lib() -> ctypes.CDLL:
         "spark_amr_fill_guardcells": (i32, [vp, vp]),
         "spark_amr_step": (i32, [vp, d, d, P(d)]),
         "spark_amr_get_time": (i32, [vp, P(d), P(i64), P(d)]),
+        "spark_amr_rank_leaves": (i32, [cp, P(CRefine), i32, i32, P(i64), P(i64)]),
+        "spark_amr_group_required_bytes": (i32, [cp, P(CRefine), i32, P(ctypes.c_size_t)]),
+        "spark_amr_init_local_group": (i32, [cp, P(CRefine), i32, i32, vp, P(vp), ctypes.c_size_t, P(vp)]),
+        "spark_amr_step_group": (i32, [P(vp), i32, d, d, P(d)]),
         "spark_fill_guardcells": (i32, [vp, vp]),
         "spark_step": (i32, [vp, d, d, P(d)]),
         "spark_advance": (i32, [vp, i64, d, i32, P(i64)]),
@@ -509,17 +514,31 @@ def amr_leaves(cfg: dict, rlo, rhi):
     return nc.value, nf.value
 
 
+def amr_rank_leaves(cfg: dict, rlo, rhi, rank: int, nranks: int):
+    """(first leaf, leaf count) of `rank` in a group of nranks."""
+    c, r = to_cconfig(cfg), _refine(rlo, rhi)
+    a, n = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().spark_amr_rank_leaves(ctypes.byref(c), ctypes.byref(r), rank, nranks, ctypes.byref(a),
+                                       ctypes.byref(n)), what="amr_rank_leaves")
+    return a.value, n.value
+
+
 class Amr:
     """A static two-level refinement (spark_amr_*): coarse blocks [rlo, rhi)
     refined by 2; state U[v][leaf][k][j][i] (coarse leaves, then fine)."""
 
-    def __init__(self, cfg: dict, rlo, rhi, device: Optional[int] = None, stream=None):
+    def __init__(self, cfg: dict, rlo, rhi, device: Optional[int] = None, stream=None, _handle=None, _arena=None,
+                 _nleaf=None):
         import torch
 
         self.torch = torch
         self.cfg = dict(cfg)
         self.device = torch.cuda.current_device() if device is None else device
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if _handle is not None:  # a member of an AmrGroup
+            self.ctx, self.arena, self.nleaf = _handle, _arena, _nleaf
+            self.shape = (cfg["ndim"] + 2, self.nleaf) + tuple(reversed(cfg["nb"]))
+            return
         nc, nf = amr_leaves(cfg, rlo, rhi)
         self.nleaf = nc + nf
         self.shape = (cfg["ndim"] + 2, self.nleaf) + tuple(reversed(cfg["nb"]))
@@ -590,3 +609,39 @@ class Amr:
             self.close()
         except Exception:
             pass
+
+
+class AmrGroup:
+    """nranks virtual ranks of a static two-level refinement on one GPU
+    (spark_amr_init_local_group / spark_amr_step_group); member r owns the
+    leaves amr_rank_leaves(cfg, rlo, rhi, r, nranks)."""
+
+    def __init__(self, cfg: dict, rlo, rhi, nranks: int, device: Optional[int] = None, stream=None):
+        import torch
+
+        device = torch.cuda.current_device() if device is None else device
+        stream = stream if stream is not None else torch.cuda.current_stream(device)
+        c, r = to_cconfig(cfg), _refine(rlo, rhi)
+        nbytes = ctypes.c_size_t()
+        _check(lib().spark_amr_group_required_bytes(ctypes.byref(c), ctypes.byref(r), nranks, ctypes.byref(nbytes)),
+               what="amr_group_required_bytes")
+        self.arenas = [torch.empty(nbytes.value, dtype=torch.uint8, device=f"cuda:{device}") for _ in range(nranks)]
+        ptrs = (ctypes.c_void_p * nranks)(*[a.data_ptr() for a in self.arenas])
+        outs = (ctypes.c_void_p * nranks)()
+        _check(lib().spark_amr_init_local_group(ctypes.byref(c), ctypes.byref(r), nranks, device,
+                                                ctypes.c_void_p(stream.cuda_stream), ptrs, nbytes.value, outs),
+               what="amr_init_local_group")
+        self.leaves = [amr_rank_leaves(cfg, rlo, rhi, q, nranks) for q in range(nranks)]
+        self.ranks = [Amr(cfg, rlo, rhi, device=device, stream=stream, _handle=ctypes.c_void_p(outs[q]),
+                          _arena=self.arenas[q], _nleaf=self.leaves[q][1]) for q in range(nranks)]
+        self._handles = (ctypes.c_void_p * nranks)(*[outs[q] for q in range(nranks)])
+
+    def step(self, dt: float = 0.0, t_end: float = 0.0, sync: bool = False):
+        d = ctypes.c_double()
+        self.ranks[0]._chk(lib().spark_amr_step_group(self._handles, len(self.ranks), dt, t_end,
+                                                      ctypes.byref(d) if sync else None), "amr_step_group")
+        return d.value if sync else None
+
+    def close(self):
+        for a in self.ranks:
+            a.close()

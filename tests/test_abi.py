@@ -176,3 +176,18 @@ def test_amr_host_plan_matches_oracle_leaf_count():
         return n.value
 
     assert nbytes((1, 1, 0), (3, 2, 2)) > nbytes((0, 0, 0), (0, 0, 0))
+
+
+def test_amr_rank_partition_covers_the_leaves():
+    """spark_amr_rank_leaves: contiguous, disjoint ranges covering every leaf."""
+    from paper_2401_03378_b200 import spark
+
+    import spark_inputs as si
+
+    p = si.Problem("a", 2, (8, 8, 1), (4, 4, 1), 2, 1, 1, 2, 0.4)
+    rlo, rhi = (1, 1, 0), (3, 3, 1)
+    n = sum(spark.amr_leaves(p.config(), rlo, rhi))
+    for nranks in (1, 2, 3, 7):
+        ranges = [spark.amr_rank_leaves(p.config(), rlo, rhi, r, nranks) for r in range(nranks)]
+        assert ranges[0][0] == 0 and sum(c for _, c in ranges) == n
+        assert all(ranges[r][0] + ranges[r][1] == ranges[r + 1][0] for r in range(nranks - 1))

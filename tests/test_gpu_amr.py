@@ -136,3 +136,26 @@ def test_failure_rolls_back(sp):
     assert a.time()[:2] == (0.0, 0)
     a.step(sync=True)
     a.close()
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 5])
+@pytest.mark.parametrize("p,rlo,rhi", [CASES[2], CASES[5], CASES[6], CASES[7]],
+                         ids=lambda x: getattr(x, "name", str(x)))
+def test_virtual_ranks_bitwise(sp, p, rlo, rhi, nranks):
+    """The leaf list split into nranks contiguous ranges: guard values and the
+    fine-face fluxBuff values cross ranks through packed exchange buffers
+    (fill_guardcells, communicate_fluxes); the result equals one rank's bit
+    for bit, with the same global dt."""
+    U0 = cons(p, si.amr_primitive(p, rlo, rhi, "random", seed=7))
+    one = sp.Amr(p.config(), rlo, rhi)
+    one.set_state(U0)
+    grp = sp.AmrGroup(p.config(), rlo, rhi, nranks)
+    for (first, count), a in zip(grp.leaves, grp.ranks):
+        a.set_state(np.ascontiguousarray(U0[:, first:first + count]))
+    for _ in range(3):
+        assert one.step(sync=True) == grp.step(sync=True)
+    ref = one.get_state()
+    for (first, count), a in zip(grp.leaves, grp.ranks):
+        assert np.array_equal(a.get_state(), ref[:, first:first + count])
+    grp.close()
+    one.close()
