@@ -9,6 +9,7 @@ O=gpurun_out/r02
 R=/tmp/r02   # ncu reports stay on the box (gpurun_out is capped at 64 MiB); summaries come back
 Q="--no-cpu-baseline --no-calibration --no-secondary --e2e-steps 1"
 run() { tag=$1; shift; timeout 600 python bench.py "$@" > $O/bench_$tag.json 2> $O/bench_$tag.err; echo "$tag rc=$?"; }
+run c4_plm
 run c4_weno --config c4_sedov3d_weno --no-calibration --no-secondary
 run c4_hybrid --riemann hybrid $Q --steps 50
 run c4_first --recon first $Q --steps 50
