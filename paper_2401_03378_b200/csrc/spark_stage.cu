@@ -86,40 +86,6 @@ __host__ __device__ constexpr bool policy_pad_ring(int ndim, int recon) {
     return ndim == 3 && recon != 2 && recon != 4;
 }
 
-// Drifting warps (one-barrier path): the per-plane CTA barrier becomes an
-// mbarrier phase (arrive after S3, wait before S4) with the z-face solve and
-// the halo conversion of plane k+2 between the two, and the 32 block-boundary
-// faces of plane k+1 solved one plane ahead by a rotating warp (k+1 mod 8), so
-// the extra solve is absorbed by the slack the other warps build up instead of
-// being paid by the whole CTA every plane.  Needs a third ring slot for first
-// order (the halo of plane k+2 is written while plane k is still read).
-#ifdef SPARK_DRIFT
-__host__ __device__ constexpr bool policy_drift(int ndim, int recon, int nbx, int nby) {
-    return policy_one_barrier(ndim, recon, nbx, nby);
-}
-#else
-__host__ __device__ constexpr bool policy_drift(int, int, int, int) { return false; }
-#endif
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "SPARK_MBAR_WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra SPARK_MBAR_WAIT_%=;\n}\n" ::"r"(a),
-        "r"(parity)
-        : "memory");
-}
-
 template <int NDIM, int RECON, int RS, int NBX, int NBY, int NBZ>
 __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(const StageArgs A) {
     constexpr bool FC = policy_face_centric(NDIM, RECON, NBX, NBY);
@@ -129,9 +95,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     constexpr int NV = NDIM + 2;
     constexpr int NG = StencilOf<RECON>::NG;
     constexpr int R = NG - 1;  // cell-centric reconstruction radius
-    constexpr bool DRIFT = policy_drift(NDIM, RECON, NBX, NBY);
-    // ring slots (planes k-R' .. k+NG alive; DRIFT: planes k .. k+2)
-    constexpr int RS_ = DRIFT ? 3 : (2 * NG - 1 > 2 ? 2 * NG - 1 : 2);
+    constexpr int RS_ = 2 * NG - 1 > 2 ? 2 * NG - 1 : 2;  // ring slots (planes k-R' .. k+NG alive)
     constexpr int RING = NDIM == 3 ? RS_ : 0;
     constexpr bool PADRING = policy_pad_ring(NDIM, RECON);
     // 3-D: the S4 operands are only prefetched into L2 in S2 and loaded in S4,
@@ -419,198 +383,6 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
 
     double* const XA0 = XA;
     double* const YA0 = YA;
-    if constexpr (DRIFT) {
-        // ------------------------------------------------ drifting warps
-        // Per plane k: S3(k) x/y faces -> arrive(k) -> z face k+1/2, halo of
-        // plane k+2 -> wait(k) -> plane k+NG into the ring, z edges of cell
-        // k+1 (+ boundary faces of plane k+1 on warp (k+1) mod 8) -> S4(k).
-        // Hazards, all ordered by one phase of `pbar` (count = all threads):
-        //  * S3(k) reads slot(k): interior committed by its owners two
-        //    (first order: one) planes earlier, halo written in the window of
-        //    k-1, both before their owners' arrive(k-1)/(k); readers passed
-        //    wait(k-1).
-        //  * the commit of plane k+NG overwrites slot(k) (3 slots) after
-        //    wait(k): every S3(k) and the boundary pass of plane k are done.
-        //  * the window's halo write into slot(k+2) = slot(k-1): its readers
-        //    (S3(k-1), boundary pass of k-1) finished before wait(k-1).
-        //  * flux buffers by plane parity: S3(k+1) and the boundary pass of
-        //    k+1 overwrite what S4(k-1) read; both run after wait(k), i.e.
-        //    after every warp's S4(k-1).
-        static_assert(PADRING && HLATE && ONEBAR, "drift path: padded ring, late halo, one-barrier layout");
-        __shared__ unsigned long long pbar;
-        double zlo[NV], zhn[NV];
-        bool zs_next = false;
-        const int warp = tid >> 5;
-        // plane k+NG of this column into the ring; z edges of cell k+1
-        auto advance = [&](int k) {
-            double w[NV];
-            ok &= cons_to_prim<NV>(pre, w, gm1);
-            if (k + 1 < nb2) load_col(k + 1 + NG, pre);
-#pragma unroll
-            for (int v = 0; v < NV; v++) ring_at(k + NG, v) = w[v];
-            zrecon(k + 1, zlo, zhn);
-            if (RS == 2) zs_next = zshock_cell(k + 1);
-        };
-        // halo cells of plane k into its slot's padding; plane k+1's in flight
-        auto halo_in = [&](int k) {
-            if (!hact) return;
-            double w[NV];
-            cp_async_wait_all();
-#pragma unroll
-            for (int v = 0; v < NV; v++) hpre[v] = hs[v * nh + hid];
-#pragma unroll
-            for (int d = 0; d < NV - 2; d++)  // reflecting-boundary image: momentum sign
-                hpre[1 + d] = __hiloint2double(__double2hiint(hpre[1 + d]) ^ (((hzf >> (1 + d)) & 1) << 31),
-                                               __double2loint(hpre[1 + d]));
-            ok &= cons_to_prim<NV>(hpre, w, gm1);
-            double* dst = ring + ((k + NG) % RS_) * NV * CP + (hcy + RO) * cw + hcx + NG;
-#pragma unroll
-            for (int v = 0; v < NV; v++) dst[v * CP] = w[v];
-            if (k + 1 < nb2) {
-                const double* src = hp + (long long)(k + 1) * (hzf >> 4);
-#pragma unroll
-                for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + hid, src + (long long)v * hvs);
-                cp_async_commit();
-            }
-        };
-        // the 32 block-boundary faces of plane k (one warp: x face 0 of rows
-        // 0-15 on lanes 0-15, y face 0 of columns 0-15 on lanes 16-31, the
-        // latter in the x frame with u_x <-> u_y swapped: bitwise identical)
-        auto boundary = [&](int k) {
-            const double* c0 = ring + ((k + NG) % RS_) * NV * CP;
-            double* const XK = XA0 + (k & 1) * NV * nb1;
-            double* const YK = YA0 + (k & 1) * NV * fyn;
-            const bool isy = (tid & 31) >= 16;
-            const int q = tid & 15;
-            const int st = isy ? cw : 1;
-            const int o = isy ? NG * cw + q + NG : (q + RO) * cw + NG;  // cell 0 of the face's line
-            double bl[NV], br[NV], fb[NV];
-            const bool bshk = shk_at(c0 + o, st, isy ? 2 : 1);
-#pragma unroll
-            for (int v = 0; v < NV; v++) {
-                const double* c = c0 + v * CP + o;
-                face_states<RECON>(c[-2 * st], c[-st], c[0], c[st], bl[v], br[v]);
-            }
-            if (RECON != 0 && !(positive(bl[0]) && positive(bl[NV - 1]) && positive(br[0]) && positive(br[NV - 1]))) {
-#pragma unroll
-                for (int v = 0; v < NV; v++) {
-                    bl[v] = c0[v * CP + o - st];
-                    br[v] = c0[v * CP + o];
-                }
-            }
-            {
-                const double l1 = bl[1], r1 = br[1];
-                bl[1] = isy ? bl[2] : l1;
-                bl[2] = isy ? l1 : bl[2];
-                br[1] = isy ? br[2] : r1;
-                br[2] = isy ? r1 : br[2];
-            }
-            face_flux<NV, RS, 0>(bl, br, bshk, gamma, gm1i, fb);
-            {
-                const double f1 = fb[1];
-                fb[1] = isy ? fb[2] : f1;
-                fb[2] = isy ? f1 : fb[2];
-            }
-#pragma unroll
-            for (int v = 0; v < NV; v++) {
-                if (isy) YK[v * fyn + q] = fb[v];
-                else XK[v * nb1 + q] = fb[v];
-            }
-        };
-
-        // prologue: plane NG into the ring, z edges of cell 1, halo of plane 1
-        advance(0);
-        if (nb2 > 1) halo_in(1);
-        if (tid == 0) mbar_init(&pbar, blockDim.x);
-        __syncthreads();  // slots of planes 0 and 1, the barrier
-        if (warp == 0) boundary(0);
-
-        for (int kk = 0; kk < nb2; kk++) {
-            const double* const cur = ring + ((kk + NG) % RS_) * NV * CP;
-            double* const XK = XA0 + (kk & 1) * NV * nb1;
-            double* const YK = YA0 + (kk & 1) * NV * fyn;
-            const long long cidx = bbase + ((long long)kk * nb1 + tj) * nb0 + ti;
-            if (a != 0.0) {
-#pragma unroll
-                for (int v = 0; v < NV; v++) asm volatile("prefetch.global.L2 [%0];" ::"l"(A.un + v * vs + cidx));
-            }
-            // ------------------------------------------------------------ S3
-            double fxo[NV];
-            {
-                double wl[NV], wr[NV], fy[NV];
-                const double* c = cur + (tj + RO) * cw + ti + NG;  // this cell
-#pragma unroll
-                for (int v = 0; v < NV; v++)
-                    face_states<RECON>(c[v * CP - 1], c[v * CP], c[v * CP + 1], c[v * CP + 2], wl[v], wr[v]);
-                if (RECON != 0 && !(positive(wl[0]) && positive(wl[NV - 1]) && positive(wr[0]) && positive(wr[NV - 1]))) {
-#pragma unroll
-                    for (int v = 0; v < NV; v++) {
-                        wl[v] = c[v * CP];
-                        wr[v] = c[v * CP + 1];
-                    }
-                }
-                face_flux<NV, RS, 0>(wl, wr, shk_at(c + 1, 1, 1), gamma, gm1i, fxo);
-#pragma unroll
-                for (int v = 0; v < NV; v++)
-                    face_states<RECON>(c[v * CP - cw], c[v * CP], c[v * CP + cw], c[v * CP + 2 * cw], wl[v], wr[v]);
-                if (RECON != 0 && !(positive(wl[0]) && positive(wl[NV - 1]) && positive(wr[0]) && positive(wr[NV - 1]))) {
-#pragma unroll
-                    for (int v = 0; v < NV; v++) {
-                        wl[v] = c[v * CP];
-                        wr[v] = c[v * CP + cw];
-                    }
-                }
-                face_flux<NV, RS, 1>(wl, wr, shk_at(c + cw, cw, 2), gamma, gm1i, fy);
-#pragma unroll
-                for (int v = 0; v < NV; v++) YK[v * fyn + (tj + 1) * nb0 + ti] = fy[v];
-            }
-            mbar_arrive(&pbar);
-            // --------------------------------------------------------- window
-            zflux(kk, zhi, zlo, zs_prev || zs_next, fzhi);
-#pragma unroll
-            for (int v = 0; v < NV; v++) zhi[v] = zhn[v];
-            zs_prev = zs_next;
-            if (kk + 2 < nb2) halo_in(kk + 2);
-            mbar_wait(&pbar, kk & 1);
-            if (kk + 1 < nb2) {
-                advance(kk + 1);
-                if (warp == ((kk + 1) & 7)) boundary(kk + 1);
-            }
-            // ------------------------------------------------------------ S4
-            double Lv[NV];
-#pragma unroll
-            for (int v = 0; v < NV; v++) {
-                const double nbr = __shfl_up_sync(0xffffffffu, fxo[v], 1);
-                const double fxm = ti == 0 ? XK[v * nb1 + tj] : nbr;
-                const double dfx = (fxo[v] - fxm) * g.rdx[0];
-                const double dfy = (YK[v * fyn + (tj + 1) * nb0 + ti] - YK[v * fyn + tj * nb0 + ti]) * g.rdx[1];
-                Lv[v] = -(dfx + dfy) - (fzhi[v] - fzlo[v]) * g.rdx[2];
-            }
-            double u0v[NV], unv[NV], un[NV];
-#pragma unroll
-            for (int v = 0; v < NV; v++) {
-                u0v[v] = __ldg(up + v * vs + cidx);
-                unv[v] = a != 0.0 ? __ldg(A.un + v * vs + cidx) : 0.0;
-            }
-            if (g.has_grav) {  // grvAccel source at U^(s-1) (CTA-uniform branch)
-                double grho = 0.0, gmg = 0.0;
-#pragma unroll
-                for (int v = 0; v < NV; v++) Lv[v] += grav_src<NV>(g, v, u0v[v], grho, gmg);
-            }
-#pragma unroll
-            for (int v = 0; v < NV; v++) {
-                const double uo = fma(bco, fma(dt, Lv[v], u0v[v]), a * unv[v]);
-                A.uout[v * vs + cidx] = uo;
-                un[v] = uo;
-                fzlo[v] = fzhi[v];
-            }
-            if (A.last) {
-                double w[NV];
-                ok &= cons_to_prim<NV>(un, w, gm1);
-                cflmin = fmin(cflmin, cfl_term<NV>(g, w));
-            }
-        }
-    } else {
     // ONEBAR: plane 0's slot (prologue ring planes + halo) must be complete
     // before S3 of plane 0; later planes are fenced by the previous S3->S4 barrier
     if (ONEBAR) __syncthreads();
@@ -1053,7 +825,6 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             }
         }
     }
-    }  // !DRIFT
     if (!ok) flag_nonphysical(A.sc);
     if (A.last) {
         __syncthreads();
@@ -1117,8 +888,7 @@ size_t stage_smem_bytes(const Geo& g, int recon) {
     const int NV = g.ndim + 2;
     const int nb0 = g.nb[0], nb1 = g.ndim >= 2 ? g.nb[1] : 1;
     const size_t P = (size_t)nb0 * nb1;
-    const bool drift = fast_shape(g) && policy_drift(g.ndim, recon, 16, 16);
-    const size_t slots = drift ? 3 : (2 * NG - 1 > 2 ? 2 * NG - 1 : 2);
+    const size_t slots = 2 * NG - 1 > 2 ? 2 * NG - 1 : 2;
     const size_t cw = nb0 + 2 * NG, ch = g.ndim >= 2 ? nb1 + 2 * NG : 1;
     const bool pad = policy_pad_ring(g.ndim, recon);
     const size_t ring = g.ndim == 3 ? slots * NV * (pad ? cw * ch : P) : 0;
