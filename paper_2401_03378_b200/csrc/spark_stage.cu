@@ -48,9 +48,11 @@ constexpr int kThreads = 256;
 // face-state arrays XB/YB, the halo edge-state pass and the S2->S3 barrier
 // disappear, and S3 solves one face at a time (no spills).
 __host__ __device__ constexpr bool policy_face_centric(int ndim, int recon, int nbx, int nby) {
-    // first order and minmod PLM (3-D +16-20 %, 2-D +12-20 %); MC measured 1 %
-    // slower, WENO5 would evaluate its edges twice
-    return nbx == 16 && nby == 16 && ndim >= 2 && recon <= 1;
+    // first order and minmod PLM (3-D +16-20 %, 2-D +12-20 %); PLM-MC with the
+    // one-barrier plane loop: 3-D 13.97 -> 17.96 G zone-updates/s (+29 %), 2-D
+    // RK2 17.30 -> 18.40 (+6 %) (alone, round 1, it was 1 % slower); WENO5
+    // would evaluate its edges twice
+    return nbx == 16 && nby == 16 && ndim >= 2 && (recon <= 1 || recon == 3);
 }
 
 template <int NV>
@@ -79,7 +81,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // plane k from overwriting fluxes that S4 of plane k-1 still reads — goes.
 // Measured on 256^3 PLM: 20.90 -> 21.38 G zone-updates/s (+2.3 %).
 __host__ __device__ constexpr bool policy_one_barrier(int ndim, int recon, int nbx, int nby) {
-    return ndim == 3 && nbx == 16 && nby == 16 && recon <= 1;
+    return ndim == 3 && nbx == 16 && nby == 16 && (recon <= 1 || recon == 3);
 }
 
 __host__ __device__ constexpr bool policy_pad_ring(int ndim, int recon) {

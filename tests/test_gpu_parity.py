@@ -73,6 +73,11 @@ STAGE_CASES = [
     si.Problem("3d_first16_hll_refl", 3, (16, 16, 16), (2, 1, 2), 1, 0, 0, 2, 0.3, bc=((1, 1), (2, 2), (0, 0))),
     si.Problem("3d_plm16_hll_reflxy", 3, (16, 16, 16), (1, 2, 2), 2, 1, 0, 3, 0.3, bc=((2, 2), (2, 1), (1, 1))),
     si.Problem("3d_plm_16x16x8", 3, (16, 16, 8), (2, 2, 2), 2, 1, 1, 2, 0.3, bc=((0, 0), (1, 1), (2, 1))),
+    # face-centric PLM-MC (one-barrier plane loop in 3-D): HLL with reflecting
+    # faces, HLLC RK3, and the 2-D plane kernel
+    si.Problem("3d_mc16_hll_refl", 3, (16, 16, 16), (2, 2, 1), 2, 3, 0, 2, 0.3, bc=((2, 2), (1, 2), (2, 2))),
+    si.Problem("3d_mc16_hllc_rk3", 3, (16, 16, 16), (1, 2, 2), 2, 3, 1, 3, 0.3, bc=((0, 0), (2, 1), (1, 1))),
+    si.Problem("2d_mc16_hllc_refl", 2, (16, 16, 1), (3, 2, 1), 2, 3, 1, 2, 0.4, bc=((2, 1), (2, 2), (1, 1))),
 ]
 
 
