@@ -12,12 +12,26 @@ Parity status per function (DESIGN.md §3 lists the pins):
   fill_guardcells  pinned: brute-force per-dimension map, index-encoded state
   prim/cons EOS    pinned: closed-form round trip, hand-computed values
   plm_face         pinned: linear exactness, extrema -> zero slope
-  weno5_edge       pinned: quadratic exactness, observed order on smooth data
+  weno5_edge       pinned: quadratic exactness, observed order on smooth data,
+                   the Jiang-Shu beta_k / omega_k written out from their
+                   definition on fixed and random stencils, ENO at a jump
+                   (JS and Z); MC: closed forms, linear exactness, order
   riemann          pinned: consistency F(W,W) = physical flux, supersonic
-                   upwinding, stationary contact, mirror antisymmetry
+                   upwinding, stationary contact, mirror antisymmetry; HLLC
+                   star flux = physical flux of the star state (Toro 10.39)
+  shock_face       pinned: sensor cases (compression / expansion / dead band),
+                   Sod flags only the shock, HLLC bitwise where nothing is flagged
   stage/step/run   pinned: exact Sod (Toro 2009, Table 4.3 Test 1),
                    conservation, uniform state, x<->y symmetry, 2-D row == 1-D,
                    advected density wave convergence order
+  step_telescoping pinned: periodic = non-telescoping bitwise, differences
+                   confined to (S-1)*NGK boundary cells, exact Sod
+  amr_*            pinned: brute-force composite guard fill, uniform state,
+                   conservation to round-off (and the correction matters),
+                   empty / full refined box = the uniform scheme, transposition
+                   symmetry, Sod through a refined half
+  tools/oracle_mutations.py: every listed mutation of this C file fails a pin
+  (profiles/r02_oracle_mutations.txt).
   Faithfulness to Flash-X Spark's own constants (limiter, eps, wave speeds):
   parity unpinned — PAPER.md prints none.
 """
