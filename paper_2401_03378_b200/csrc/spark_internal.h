@@ -3,7 +3,6 @@
 #pragma once
 
 #include <cstdint>
-#include <cuda.h>  // CUtensorMap (KB1's TMA halo strips)
 #include <cuda_runtime.h>
 
 namespace spark {
@@ -70,10 +69,6 @@ struct StageArgs {
     int honor_active;             // 1: copy-through when sc->active == 0
     int part;                     // 0 all blocks; 1 blocks touching no exchanged rank face
                                   // ("interior", run while halos travel); 2 the others
-    // KB1 halo strips by TMA (3-D 16^3 PLM / MC): tensor maps of uprev as
-    // [block][v][z][y][x] with an x-strip box (2x16) and a y-strip box (16x2);
-    // encoded by launch_stage, never by the caller
-    CUtensorMap tm[2];
 };
 
 // Telescoping through HBM tiles (spark_telescope_tile.cu): G = S*NGK guard

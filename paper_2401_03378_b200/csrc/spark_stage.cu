@@ -88,54 +88,8 @@ __host__ __device__ constexpr bool policy_pad_ring(int ndim, int recon) {
     return ndim == 3 && recon != 2 && recon != 4;
 }
 
-// Halo strips by TMA (3-D 16x16x16, NG = 2: PLM / MC): the four face-halo
-// strips of the next plane (x: 2 columns x 16 rows of the left / right
-// neighbour block, y: 16 columns x 2 rows of the lower / upper one, all NV
-// variables) arrive as one cp.async.bulk.tensor box each, issued by lane 0 of
-// the strip's warp (warps 4-7 own one strip each, see HLATE) and completed on
-// the strip's mbarrier; strips whose neighbour is not a block of this sub-box
-// (physical boundary, rank halo) keep the per-cell cp.async gather.
-__host__ __device__ constexpr bool policy_tma_halo(int ndim, int recon, int nbx, int nby) {
-#ifdef SPARK_NO_TMA_HALO
-    return false;
-#else
-    return ndim == 3 && nbx == 16 && nby == 16 && (recon == 1 || recon == 3);
-#endif
-}
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "SPARK_MBAR_WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra SPARK_MBAR_WAIT_%=;\n}\n" ::"r"(a),
-        "r"(parity)
-        : "memory");
-}
-// one [block][v][z][y][x] box of the tensor map into shared memory
-__device__ __forceinline__ void tma_box5(double* dst, const CUtensorMap* tm, int x, int y, int z, int b,
-                                         unsigned long long* bar) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    const unsigned m = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(d),
-        "l"(tm), "r"(x), "r"(y), "r"(z), "r"(0), "r"(b), "r"(m)
-        : "memory");
-}
-
 template <int NDIM, int RECON, int RS, int NBX, int NBY, int NBZ>
-__global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(const __grid_constant__ StageArgs A) {
+__global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(const StageArgs A) {
     constexpr bool FC = policy_face_centric(NDIM, RECON, NBX, NBY);
     // paired face solves in S3 (WENO5 / MC); the face-centric path solves one
     // face at a time (paired, its reconstruction temporaries spill: -9 %)
@@ -194,11 +148,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     // FC in 3-D: the next plane's raw halo cells arrive by cp.async in shared
     // memory (no prefetch registers held across the plane)
     constexpr bool HSM = FC && NDIM == 3;
-    // halo strips by TMA (with HLATE below: HSM && PADRING)
-    constexpr bool TMAH = HSM && PADRING && NG == 2 && policy_tma_halo(NDIM, RECON, NBX, NBY);
-    // [NV][nh]; TMAH: [strip][NV][32] (one TMA box per strip), 128-B aligned
-    double* hs = YB + (FC ? 0 : NV * fyn);
-    if (TMAH) hs = (double*)(((uintptr_t)hs + 127) & ~(uintptr_t)127);
+    double* hs = YB + (FC ? 0 : NV * fyn);     // [NV][nh]
 
     const double dt = A.dt_ptr ? *A.dt_ptr : A.dt_value;
     const double a = A.a, bco = A.b;
@@ -377,33 +327,6 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     const int hid = HLATE ? tid - (P - nh) : tid;  // halo cell of this thread
     int hcx = 0, hcy = 0;
     double hpre[NV];
-    // staging slot of variable v of halo cell h
-    auto hsx = [&](int v, int h) -> double* {
-        return TMAH ? hs + (h >> 5) * NV * 32 + v * 32 + (h & 31) : hs + v * nh + h;
-    };
-    // TMAH: this warp's strip (0 x-, 1 x+, 2 y-, 3 y+: halo cells 32s..32s+31,
-    // the layout of the TMA box), its neighbour block if that is a block of
-    // this sub-box (else -1: per-cell gather), and the box origin in it
-    __shared__ unsigned long long hbar[4];
-    const int strip = hid >> 5;
-    int snb = -1, sx0 = 0, sy0 = 0;
-    if (TMAH && hact) {
-        int qx = bx, qy = by;
-        if (strip == 0) { qx = bx - 1; sx0 = nb0 - NG; }
-        if (strip == 1) qx = bx + 1;
-        if (strip == 2) { qy = by - 1; sy0 = nb1 - NG; }
-        if (strip == 3) qy = by + 1;
-        if (qx >= 0 && qx < g.bn[0] && qy >= 0 && qy < g.bn[1]) snb = qx + g.bn[0] * (qy + g.bn[1] * bz);
-    }
-    const bool stma = TMAH && hact && snb >= 0;  // warp-uniform
-    constexpr unsigned kStripBytes = 32u * NV * sizeof(double);
-    auto strip_load = [&](int z) {  // lane 0: TMA box of plane z into the strip's staging
-        if ((tid & 31) == 0) {
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // after the generic reads
-            mbar_expect_tx(&hbar[strip], kStripBytes);
-            tma_box5(hs + strip * NV * 32, &A.tm[strip >> 1], sx0, sy0, z, snb, &hbar[strip]);
-        }
-    };
     // Per-plane sources resolved once: a halo cell in a face-neighbour block of
     // this sub-box is a plain column (stride P per plane) of that block; others
     // (physical boundary / received slab) take the general gather every plane.
@@ -428,14 +351,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 ok &= cons_to_prim<NV>(hpre, w, gm1);
 #pragma unroll
                 for (int v = 0; v < NV; v++) ring[((NG % RS_) * NV + v) * CP + (hcy + RO) * cw + hcx + NG] = w[v];
-                if (stma) {
-                    if ((tid & 31) == 0) mbar_init(&hbar[strip], 1);
-                    __syncwarp();
-                    if (nb2 > 1) strip_load(1);
-                } else if (nb2 > 1) {
+                if (nb2 > 1) {
                     const double* src = hp + (hzf >> 4);
 #pragma unroll
-                    for (int v = 0; v < NV; v++) cp_async8(hsx(v, hid), src + (long long)v * hvs);
+                    for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + hid, src + (long long)v * hvs);
                     cp_async_commit();
                 }
             } else if (HSM) {
@@ -540,10 +459,9 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
         // ---------------------------------------------------------------- S2
         if (HLATE && hact && kk + 1 < nb2) {  // halo of plane kk+1 -> its slot
             double w[NV];
-            if (stma) mbar_wait(&hbar[strip], kk & 1);  // box of plane kk+1 (issued a plane ago)
-            else cp_async_wait_all();  // no-op: complete since S4 of the previous plane
+            cp_async_wait_all();  // no-op: complete since S4 of the previous plane
 #pragma unroll
-            for (int v = 0; v < NV; v++) hpre[v] = *hsx(v, hid);
+            for (int v = 0; v < NV; v++) hpre[v] = hs[v * nh + hid];
 #pragma unroll
             for (int d = 0; d < NV - 2; d++)  // reflecting-boundary image: momentum sign
                 hpre[1 + d] = __hiloint2double(__double2hiint(hpre[1 + d]) ^ (((hzf >> (1 + d)) & 1) << 31),
@@ -553,15 +471,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
 #pragma unroll
             for (int v = 0; v < NV; v++) nxt[v * CP] = w[v];
             if (kk + 2 < nb2) {
-                if (stma) {
-                    __syncwarp();  // every lane has read the strip
-                    strip_load(kk + 2);
-                } else {
-                    const double* src = hp + (long long)(kk + 2) * (hzf >> 4);
+                const double* src = hp + (long long)(kk + 2) * (hzf >> 4);
 #pragma unroll
-                    for (int v = 0; v < NV; v++) cp_async8(hsx(v, hid), src + (long long)v * hvs);
-                    cp_async_commit();
-                }
+                for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + hid, src + (long long)v * hvs);
+                cp_async_commit();
             }
         }
         // operands of the S4 update, requested now so the loads overlap S2/S3
@@ -926,45 +839,6 @@ cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiled encode_tiled() {
-    static EncodeTiled fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            p = nullptr;
-        return reinterpret_cast<EncodeTiled>(p);
-    }();
-    return fn;
-}
-
-// the two halo-strip maps of uprev ([block][v][z][y][x], fp64): box 2x16 / 16x2
-cudaError_t encode_halo_maps(StageArgs& a) {
-    const EncodeTiled enc = encode_tiled();
-    if (!enc) return cudaErrorNotSupported;
-    const Geo& g = a.g;
-    const cuuint64_t nblk = (cuuint64_t)g.bn[0] * g.bn[1] * g.bn[2];
-    const cuuint64_t dims[5] = {(cuuint64_t)g.nb[0], (cuuint64_t)g.nb[1], (cuuint64_t)g.nb[2],
-                                (cuuint64_t)g.nvar, nblk};
-    const cuuint64_t cpb = (cuuint64_t)g.nb[0] * g.nb[1] * g.nb[2];
-    const cuuint64_t strides[4] = {8ull * g.nb[0], 8ull * g.nb[0] * g.nb[1], 8ull * cpb, 8ull * cpb * g.nvar};
-    const cuuint32_t ones[5] = {1, 1, 1, 1, 1};
-    constexpr cuuint32_t ng = 2;  // strip depth: NG of PLM / MC (the only TMAH cases)
-    const cuuint32_t box[2][5] = {{ng, (cuuint32_t)g.nb[1], 1, (cuuint32_t)g.nvar, 1},
-                                  {(cuuint32_t)g.nb[0], ng, 1, (cuuint32_t)g.nvar, 1}};
-    for (int m = 0; m < 2; m++) {
-        const CUresult r = enc(&a.tm[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(a.uprev), dims,
-                               strides, box[m], ones, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    }
-    return cudaSuccess;
-}
-
 template <int NDIM, int RECON, int RS, int NBX, int NBY, int NBZ>
 cudaError_t launch_t(const StageArgs& a, cudaStream_t s) {
     const size_t smem = stage_smem_bytes(a.g, RECON);
@@ -972,13 +846,7 @@ cudaError_t launch_t(const StageArgs& a, cudaStream_t s) {
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
     const long long nblk = (long long)a.g.bn[0] * a.g.bn[1] * a.g.bn[2];
-    if constexpr (NBZ == 16 && policy_tma_halo(NDIM, RECON, NBX, NBY)) {
-        StageArgs b = a;
-        if ((e = encode_halo_maps(b)) != cudaSuccess) return e;
-        k<<<(unsigned)nblk, stage_block_threads(a.g, RECON), smem, s>>>(b);
-    } else {
-        k<<<(unsigned)nblk, stage_block_threads(a.g, RECON), smem, s>>>(a);
-    }
+    k<<<(unsigned)nblk, stage_block_threads(a.g, RECON), smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -1034,8 +902,7 @@ size_t stage_smem_bytes(const Geo& g, int recon) {
     const size_t fy = g.ndim >= 2 ? (onebar ? 2 : nst) * NV * (size_t)nb0 * (nb1 + 1) : 0;
     const size_t nh = 2 * (size_t)NG * (nb0 + nb1);
     const size_t hsm = k16 && g.ndim == 3 && nst == 1 ? NV * nh : 0;  // HSM staging
-    const size_t tmah = k16 && policy_tma_halo(g.ndim, recon, 16, 16) ? 16 : 0;  // 128-B alignment of it
-    return (ring + cur + fx + fy + hsm + tmah) * sizeof(double);
+    return (ring + cur + fx + fy + hsm) * sizeof(double);
 }
 
 cudaError_t launch_stage(const StageArgs& a, int recon, int riemann, cudaStream_t s) {
