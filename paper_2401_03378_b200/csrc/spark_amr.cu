@@ -1195,6 +1195,7 @@ spark_status spark_amr_step_group(spark_amr* const* amrs, int32_t n, double dt, 
     spark_amr* a0 = amrs[0];
     return amr_guard(a0, [&] {
         if (!a0->group || (int)a0->group->size() != n) throw AmrError(SPARK_ERR_ARG, "needs all members of one group");
+        if (n != a0->nranks) throw AmrError(SPARK_ERR_STATE, "a member of this group was finalized");
         ACU(cudaSetDevice(a0->device));
         std::vector<spark_amr*> m(*a0->group);
         std::vector<int> old;

@@ -872,6 +872,14 @@ spark_status spark_finalize(spark_ctx* ctx) {
 
 const char* spark_last_error(const spark_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+// the members of c's local group, all of them (a finalized member leaves a
+// group that can no longer exchange or step)
+static const std::vector<spark_ctx*>& group_members(const spark_ctx* c) {
+    const auto& m = c->group->members;
+    if ((int)m.size() != c->nranks) throw Error(SPARK_ERR_STATE, "a member of this local group was finalized");
+    return m;
+}
+
 static void after_state_loaded(spark_ctx* c) {
     launched(c, spark::launch_scalars_reset(c->sc, c->stream), "scalars reset");
     launched(c, spark::launch_cfl_min(c->plan.geo, c->U[c->n_idx], c->sc, c->stream), "cfl min");
@@ -968,8 +976,8 @@ spark_status spark_fill_guardcells(spark_ctx* ctx, double* padded_out) {
         if (!ctx->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
         set_device(ctx);
         if (ctx->group) {
-            for (spark_ctx* m : ctx->group->members) pack_all(m, m->U[m->n_idx]);
-            exchange_local(ctx->group->members);
+            for (spark_ctx* m : group_members(ctx)) pack_all(m, m->U[m->n_idx]);
+            exchange_local(group_members(ctx));
         } else if (ctx->comm) {
             pack_all(ctx, ctx->U[ctx->n_idx]);
             exchange_nccl(ctx, ctx->stream);
@@ -1035,7 +1043,7 @@ spark_status spark_step_group(spark_ctx* const* ctxs, int32_t n, double dt, doub
     return guard(c0, [&] {
         if (!c0->group || (int)c0->group->members.size() != n)
             throw Error(SPARK_ERR_ARG, "spark_step_group needs all contexts of one local group");
-        std::vector<spark_ctx*> m(c0->group->members);
+        std::vector<spark_ctx*> m(group_members(c0));
         for (spark_ctx* c : m)
             if (!c->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
         set_device(c0);
@@ -1326,7 +1334,7 @@ extern "C" spark_status spark_step_group_telescoping(spark_ctx* const* ctxs, int
     return guard(c0, [&] {
         if (!c0->group || (int)c0->group->members.size() != n)
             throw Error(SPARK_ERR_ARG, "needs all contexts of one local group");
-        std::vector<spark_ctx*> m(c0->group->members);
+        std::vector<spark_ctx*> m(group_members(c0));
         for (spark_ctx* c : m) {
             if (!c->have_state) throw Error(SPARK_ERR_STATE, "no state loaded");
             if (!c->tiles.ready) throw Error(SPARK_ERR_STATE, "telescoping tiles need spark_set_scratch first");

@@ -137,3 +137,33 @@ def test_resume_is_bitwise(sp, name):
     tc, nc, _ = c.time()
     assert (tc, nc) == (ta, na)
     assert np.array_equal(c.get_state().cpu().numpy(), a.get_state().cpu().numpy())
+
+
+def test_group_with_a_finalized_member_refuses_to_step(sp):
+    """Finalizing one member of a local group leaves the others unable to
+    exchange: stepping or filling guards on what is left is a state error,
+    not a silent exchange with a missing rank."""
+    import ctypes
+
+    cfg = P2.config()
+    grp = sp.LocalGroup(cfg, 2)
+    G0 = si.to_global(P2, colliding_state(P2, 0.55, 0.7))
+    for r, s in enumerate(grp.ranks):
+        s.set_state(local(P2, G0, cfg, sp, r, 2))
+    h0 = grp._handles[0]
+    grp.ranks[1].close()
+    st = sp.lib().spark_step_group((ctypes.c_void_p * 1)(h0), 1, 1e-5, 0.0, None)
+    assert st == sp.SPARK_ERR_STATE
+    assert "finalized" in sp.lib().spark_last_error(ctypes.c_void_p(h0)).decode()
+    with pytest.raises(sp.SparkError, match="finalized"):
+        grp.ranks[0].fill_guardcells()
+    grp.ranks[0].close()
+
+    p = si.Problem("g", 2, (8, 8, 1), (4, 4, 1), 2, 1, 1, 2, 0.4, bc=((0, 0), (0, 0), (1, 1)))
+    rlo, rhi = (1, 1, 0), (3, 3, 1)
+    ag = sp.AmrGroup(p.config(), rlo, rhi, 2)
+    h0 = ag._handles[0]
+    ag.ranks[1].close()
+    st = sp.lib().spark_amr_step_group((ctypes.c_void_p * 1)(h0), 1, 1e-5, 0.0, None)
+    assert st == sp.SPARK_ERR_STATE
+    ag.ranks[0].close()
