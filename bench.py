@@ -177,6 +177,22 @@ def problem_for(args, world: int) -> si.Problem:
     return p
 
 
+def exchange_info(p) -> dict:
+    """What the --self-exchange line moves per stage, and the wire time the same
+    slabs would take between two B200s (B200_PROFILING.md: 770 GB/s measured
+    peer copy per direction) — the part a one-GPU run cannot show."""
+    cn = [p.nb[d] * p.nblk[d] for d in range(3)]
+    slab_cells = [p.ng * int(np.prod([cn[e] for e in range(3) if e != d])) for d in range(p.ndim)]
+    per_stage = 2 * p.nvar * 8 * sum(slab_cells)  # sent (= received) bytes per stage
+    inner = int(np.prod([max(p.nblk[d] - 2, 0) for d in range(p.ndim)]))
+    return {"path": "pack -> ncclSend/ncclRecv (to itself, the production message order) on the comm stream "
+                    "-> interior blocks while the slabs travel -> boundary blocks read the received slabs; "
+                    "u64 ncclAllReduce of (CFL min, failure word) per step",
+            "faces": 2 * p.ndim, "bytes_per_stage": per_stage,
+            "nvlink_us_per_stage_est": per_stage / 770e9 * 1e6,
+            "interior_block_share": inner / int(np.prod(p.nblk[:p.ndim]))}
+
+
 # ------------------------------------------------------ secondary workload
 def secondary_run(name: str, steps: int, warmup: int, local: int) -> dict:
     """The other scheme of BASELINE configs[3] (which does not name the
@@ -410,6 +426,12 @@ def main():
     ap.add_argument("--shock-thresh", type=float, default=0.5, help="shockDet threshold for --riemann hybrid")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = the config's grid per GPU; strong = the config's grid split over N")
+    ap.add_argument("--periodic", action="store_true",
+                    help="every face periodic, wrapped inside the kernel (the reference point of --self-exchange)")
+    ap.add_argument("--self-exchange", action="store_true",
+                    help="N=1: periodic faces through the multi-rank path (pack -> ncclSend/Recv to itself -> "
+                         "interior/boundary launches) every stage: the per-rank exchange machinery of an interior "
+                         "rank, measured on one GPU")
     ap.add_argument("--amr", action="store_true",
                     help="NEXT N3: time the static two-level refinement (spark_amr_step) on the config's grid "
                          "with its central quarter of blocks per dimension refined (one GPU)")
@@ -438,12 +460,19 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     p = problem_for(args, world)
+    selfx = args.self_exchange and world == 1
+    if selfx:  # every face periodic: all six go through NCCL (the faces of an interior rank)
+        p = p.with_(name=p.name + "+selfx", bc=((0, 0),) * 3)
+    elif args.periodic:
+        p = p.with_(name=p.name + "+periodic", bc=((0, 0),) * 3)
     cfg = p.config()
     nccl_id = None
     if world > 1:
         obj = [spark.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+    elif selfx:
+        nccl_id = spark.nccl_unique_id()
 
     stream = torch.cuda.Stream()
     lo, n = spark.rank_box(cfg, rank, world)
@@ -513,7 +542,8 @@ def main():
         bytes_per_launch = bytes_per_step_local / p.rk_stages
     avg_launch_s = stage_ms * 1e-3 / max(stage_launches, 1)
     achieved = bytes_per_launch / avg_launch_s / 1e9
-    traffic = ncu_traffic(p.name)
+    ncu_name = p.name.replace("+selfx", "").replace("+periodic", "")  # the plain run's kernel instantiation
+    traffic = ncu_traffic(ncu_name)
     traffic_note = None
     if traffic is None and p.name.startswith("c5_"):
         # configs[4] runs the same kernel instantiation as configs[3] (16^3 blocks):
@@ -532,7 +562,7 @@ def main():
     # per zone-update (ncu, profiles/ncu_summary.json) x the kernel's zone rate,
     # against the measured DFMA issue rate (tools/fp64_peak.cu, profiles/fp64_peak.json)
     roofline_fp64 = None
-    fp64_per_zone = ncu_field(p.name, "fp64_inst_per_zone") or ncu_field(p.name.replace("c5_", "c4_"),
+    fp64_per_zone = ncu_field(ncu_name, "fp64_inst_per_zone") or ncu_field(ncu_name.replace("c5_", "c4_"),
                                                                            "fp64_inst_per_zone")
     fp64_peak = fp64_peak_rate()
     if fp64_per_zone and fp64_peak:
@@ -548,7 +578,7 @@ def main():
     # zone rate, against the SM issue peak (4 schedulers x 1 warp-instr/clk x 148
     # SMs at the sampled clock; B200_PROFILING.md unit counts)
     roofline_issue = None
-    inst_per_zone = ncu_field(p.name, "inst_per_zone") or ncu_field(p.name.replace("c5_", "c4_"), "inst_per_zone")
+    inst_per_zone = ncu_field(ncu_name, "inst_per_zone") or ncu_field(ncu_name.replace("c5_", "c4_"), "inst_per_zone")
     if inst_per_zone:
         zu_rate_kernel = cells_local * p.rk_stages * args.steps / (stage_ms * 1e-3)
         clk_hz = (statistics.median(clk.samples) if clk.samples else 1965.0) * 1e6
@@ -687,7 +717,7 @@ def main():
     clocks = clk.summary()
     secondary = None
     if rank == 0 and world == 1 and args.config == "c4_sedov3d_plm" and not args.no_secondary and \
-            not (args.recon or args.riemann or args.grav or args.telescoping or args.graphs):
+            not (args.recon or args.riemann or args.grav or args.telescoping or args.graphs or args.self_exchange or args.periodic):
         secondary = secondary_run("c4_sedov3d_weno", 10, 3, local)
     if rank == 0:
         line = {
@@ -703,6 +733,7 @@ def main():
                        "launch": "cuda-graph (spark_run)" if args.graphs else "stream (spark_step)"},
             "roofline": roofline, "roofline_fp64": roofline_fp64, "roofline_issue": roofline_issue, "hbm_calibration_gbs": calib,
             "cpu_baseline": cpu, "e2e": e2e,
+            "exchange": exchange_info(p) if selfx else None,
             "gpu_launches": total_launches,
             "clocks": clocks,
             "secondary": secondary,
