@@ -208,12 +208,19 @@ def _oracle_subbox_step(p, G, lo, hi, margin, dt):
     return R[:, lo[2] - elo[2]:hi[2] - elo[2], lo[1] - elo[1]:hi[1] - elo[1], lo[0] - elo[0]:hi[0] - elo[0]]
 
 
-@pytest.mark.parametrize("name", ["c4_sedov3d_plm", "c4_sedov3d_weno"])
+C4_VARIANTS = {  # the bench's --recon / --riemann lines: same grid, other kernel instantiations
+    "c4_sedov3d_plm": {}, "c4_sedov3d_weno": {},
+    "c4_sedov3d_plm+mc": {"recon": 3}, "c4_sedov3d_plm+first": {"recon": 0},
+    "c4_sedov3d_plm+hybrid": {"riemann": si.RIEMANN_HYBRID, "shock_thresh": 0.5},
+}
+
+
+@pytest.mark.parametrize("name", sorted(C4_VARIANTS))
 def test_c4_sedov3d_sampled(sp, name):
     """configs[3] at full size (256^3 in 16^3 blocks) in the launch configuration
     bench.py times: one GPU step with the CFL dt; sampled sub-boxes (the blast
     centre, a domain corner, a block-boundary slab) recomputed by the oracle."""
-    p = si.PRESETS[name]
+    p = si.PRESETS[name.split("+")[0]].with_(**C4_VARIANTS[name])
     U0 = cons(p, si.initial_primitive(p))
     dt_o = oracle.dt(p.config(), U0)
     s = make(sp, p, U=U0)
