@@ -17,6 +17,10 @@ LIB = os.path.join(LIBDIR, "libspark.so")
 # parity build: no FMA contraction, IEEE division / sqrt (R15/R16)
 STRICT_LIB = os.path.join(LIBDIR, "libspark_strict.so")
 STRICT_FLAGS = ("--fmad=false", "-DSPARK_STRICT_MATH")
+# checked build: KB1's shared / global addresses and the halo-source mapping
+# asserted in range (a trap on violation); compute-sanitizer is closed on the pool
+CHECKED_LIB = os.path.join(LIBDIR, "libspark_checked.so")
+CHECKED_FLAGS = ("-DSPARK_CHECKED",)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -62,6 +66,22 @@ def build_strict(force: bool = False) -> str:
     return build(force=True, out=STRICT_LIB, flags=STRICT_FLAGS)
 
 
+def build_checked(force: bool = False) -> str:
+    """libspark_checked.so: the same sources with -DSPARK_CHECKED."""
+    if not force and not stale_lib(CHECKED_LIB):
+        return CHECKED_LIB
+    return build(force=True, out=CHECKED_LIB, flags=CHECKED_FLAGS)
+
+
+def build_all(force: bool = False) -> list:
+    """The production, strict and checked libraries, compiled concurrently."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(3) as ex:
+        jobs = [ex.submit(build, force), ex.submit(build_strict, force), ex.submit(build_checked, force)]
+        return [j.result() for j in jobs]
+
+
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defs=(), flags=()) -> str:
     """Build libspark.so (``out``/``defs``: design-experiment variants, tools/ablate.sh)."""
     if out == LIB and not force and not stale():
@@ -83,5 +103,9 @@ if __name__ == "__main__":
     outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
     if "--strict" in sys.argv:
         print(build_strict(force="--force" in sys.argv))
+    elif "--checked" in sys.argv:
+        print(build_checked(force="--force" in sys.argv))
+    elif "--all" in sys.argv:
+        print("\n".join(build_all(force="--force" in sys.argv)))
     else:
         print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=outs[0] if outs else LIB, defs=defs))

@@ -489,6 +489,9 @@ __device__ __forceinline__ bool fetch_src(const Geo& g, const double* __restrict
         const int e0 = hd == 0 ? g.ng : g.cn[0];
         const int e1 = hd == 1 ? g.ng : g.cn[1];
         idx = ((long long)c[2] * e1 + c[1]) * e0 + c[0];
+#ifdef SPARK_CHECKED  // the cell lies in the received slab (SPARK_CHECKED: spark_stage.cu)
+        if (idx < 0 || idx >= g.slab[hd] || !halo[hd][hs]) __trap();
+#endif
         src.p = halo[hd][hs] + idx;
         src.vs = g.slab[hd];
     } else {
@@ -496,6 +499,10 @@ __device__ __forceinline__ bool fetch_src(const Geo& g, const double* __restrict
         const long long blk = bx + (long long)g.bn[0] * (by + (long long)g.bn[1] * bz);
         idx = blk * g.bs + ((long long)(l[2] - bz * g.nb[2]) * g.nb[1] + (l[1] - by * g.nb[1])) * g.nb[0] +
               (l[0] - bx * g.nb[0]);
+#ifdef SPARK_CHECKED  // the mapped cell lies in the sub-box
+        for (int d = 0; d < 3; d++)
+            if (l[d] < 0 || l[d] >= g.cn[d]) __trap();
+#endif
         src.p = u + idx;
         src.vs = g.vs;
     }

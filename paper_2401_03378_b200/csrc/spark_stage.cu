@@ -68,6 +68,20 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+// Checked build (-DSPARK_CHECKED, libspark_checked.so; compute-sanitizer is
+// closed on the GPU pool): every shared-memory address KB1 forms is asserted
+// inside the launch's dynamic shared memory and every global address inside
+// one of the launch's buffers (U^(s-1), U^n, the output, the received
+// slabs); a violation traps (the launch fails with an illegal-instruction
+// error). Production builds compile the checks away.
+#ifdef SPARK_CHECKED
+#define SCHK(p) schk_(p)
+#define GCHK(p) gchk_(p)
+#else
+#define SCHK(p) ((void)0)
+#define GCHK(p) ((void)0)
+#endif
+
 // Padded ring (3-D, reconstruction half-width <= 2): the ring slots of the
 // z-march are whole padded planes [NV][(nb1+2NG)][(nb0+2NG)], so the slot of
 // plane k IS the x/y working plane of plane k (its halo cells are written into
@@ -114,6 +128,22 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     constexpr int RO = NDIM >= 2 ? NG : 0;  // row offset of the interior in cur
     const Geo& g = A.g;
     extern __shared__ double smem[];
+#ifdef SPARK_CHECKED
+    unsigned dsz_;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsz_));
+    auto schk_ = [&](const double* p) {
+        if (p < smem || p >= smem + dsz_ / sizeof(double)) __trap();
+    };
+    const long long nst_ = (long long)g.nvar * g.ncell;
+    auto gchk_ = [&](const double* p) {
+        bool in = (p >= A.uprev && p < A.uprev + nst_) || (A.un && p >= A.un && p < A.un + nst_) ||
+                  (p >= A.uout && p < A.uout + nst_);
+        for (int d = 0; d < 3; d++)
+            for (int e = 0; e < 2; e++)
+                in |= A.halo[d][e] && p >= A.halo[d][e] && p < A.halo[d][e] + (long long)g.nvar * g.slab[d];
+        if (!in) __trap();
+    };
+#endif
 
     const int nb0 = NBX ? NBX : g.nb[0];
     const int nb1 = NDIM >= 2 ? (NBY ? NBY : g.nb[1]) : 1;
@@ -166,7 +196,11 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             for (int kk = 0; kk < nb2; kk++) {
                 const long long idx = bbase + ((long long)kk * nb1 + tj) * nb0 + ti;
 #pragma unroll
-                for (int v = 0; v < NV; v++) A.uout[v * vs + idx] = up[v * vs + idx];
+                for (int v = 0; v < NV; v++) {
+                    GCHK(A.uout + v * vs + idx);
+                    GCHK(up + v * vs + idx);
+                    A.uout[v * vs + idx] = up[v * vs + idx];
+                }
             }
         return;
     }
@@ -187,8 +221,11 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
         if (d == 1) { q1 += side ? 1 : -1; inside = q1 >= 0 && q1 < g.bn[1]; }
         if (d == 2) { q2 += side ? 1 : -1; inside = q2 >= 0 && q2 < g.bn[2]; }
         if (d < 0) {
+            GCHK(up + bbase + off);
+            GCHK(up + bbase + off + (NV - 1) * vs);
             ldg_cons<NV>(up + bbase + off, vs, u);
         } else if (inside) {
+            GCHK(up + (q0 + (long long)g.bn[0] * (q1 + (long long)g.bn[1] * q2)) * bs + off + (NV - 1) * vs);
             ldg_cons<NV>(up + (q0 + (long long)g.bn[0] * (q1 + (long long)g.bn[1] * q2)) * bs + off, vs, u);
         } else {
             fetch_cons<NV>(g, up, A.halo, cx0 + x, cy0 + y, cz0 + z, u);
@@ -202,8 +239,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
 
     // z machinery (3-D): ring slot of plane z is (z + NG) mod RS_
     auto ring_at = [&](int z, int v) -> double& {
-        if (PADRING) return ring[(((z + NG) % RS_) * NV + v) * CP + (tj + RO) * cw + ti + NG];
-        return ring[(((z + NG) % RS_) * NV + v) * P + tid];
+        double& r = PADRING ? ring[(((z + NG) % RS_) * NV + v) * CP + (tj + RO) * cw + ti + NG]
+                            : ring[(((z + NG) % RS_) * NV + v) * P + tid];
+        SCHK(&r);
+        return r;
     };
     double zhi[NV];   // L state of the face above the current plane (top edge of cell kk)
     double fzlo[NV];  // flux through the face below the current plane
@@ -262,6 +301,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             double u[4], pr[4], r[4];
 #pragma unroll
             for (int m = 0; m < 4; m++) {
+                SCHK(c + (NV - 1) * CP + (m - 2) * st);
+                SCHK(c + (m - 2) * st);
                 u[m] = c[vn * CP + (m - 2) * st];
                 pr[m] = c[(NV - 1) * CP + (m - 2) * st];
                 r[m] = c[(m - 2) * st];
@@ -347,35 +388,57 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             hzf = (int)((s1.p - s0.p) * 16) | s0.flip;
             if (HLATE) {  // plane 0 now (into its slot's padding), plane 1 in flight
                 double w[NV];
+                GCHK(hp);
+                GCHK(hp + (long long)(NV - 1) * hvs);
                 load_src<NV>(hp, hvs, s0.flip, hpre);
                 ok &= cons_to_prim<NV>(hpre, w, gm1);
 #pragma unroll
-                for (int v = 0; v < NV; v++) ring[((NG % RS_) * NV + v) * CP + (hcy + RO) * cw + hcx + NG] = w[v];
+                for (int v = 0; v < NV; v++) {
+                    SCHK(&ring[((NG % RS_) * NV + v) * CP + (hcy + RO) * cw + hcx + NG]);
+                    ring[((NG % RS_) * NV + v) * CP + (hcy + RO) * cw + hcx + NG] = w[v];
+                }
                 if (nb2 > 1) {
                     const double* src = hp + (hzf >> 4);
 #pragma unroll
-                    for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + hid, src + (long long)v * hvs);
+                    for (int v = 0; v < NV; v++) {
+                        SCHK(hs + v * nh + hid);
+                        GCHK(src + (long long)v * hvs);
+                        cp_async8(hs + v * nh + hid, src + (long long)v * hvs);
+                    }
                     cp_async_commit();
                 }
             } else if (HSM) {
 #pragma unroll
-                for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + tid, hp + (long long)v * hvs);
+                for (int v = 0; v < NV; v++) {
+                    SCHK(hs + v * nh + tid);
+                    GCHK(hp + (long long)v * hvs);
+                    cp_async8(hs + v * nh + tid, hp + (long long)v * hvs);
+                }
                 cp_async_commit();
             } else {
+                GCHK(hp + (long long)(NV - 1) * hvs);
                 load_src<NV>(hp, hvs, s0.flip, hpre);
             }
         } else {  // one plane: a single load through the block-neighbour fast path
             load_cons(hcx, hcy, 0, hpre);
         }
     }
-    auto load_halo = [&](int z, double* u) { load_src<NV>(hp + (long long)z * (hzf >> 4), hvs, hzf & 15, u); };
+    auto load_halo = [&](int z, double* u) {
+        GCHK(hp + (long long)z * (hzf >> 4) + (long long)(NV - 1) * hvs);
+        load_src<NV>(hp + (long long)z * (hzf >> 4), hvs, hzf & 15, u);
+    };
     // this column: planes z < nb2 of the own block, z >= nb2 of the block above
     // (if inside the sub-box, else the general gather)
     const double* csrc = up + bbase + (long long)tj * nb0 + ti;
     const double* casrc = (NDIM == 3 && bz + 1 < g.bn[2]) ? csrc + (long long)g.bn[0] * g.bn[1] * bs : nullptr;
     auto load_col = [&](int z, double* u) {
-        if (z < nb2) ldg_cons<NV>(csrc + (long long)z * P, vs, u);
-        else if (casrc) ldg_cons<NV>(casrc + (long long)(z - nb2) * P, vs, u);
+        if (z < nb2) {
+            GCHK(csrc + (long long)z * P + (NV - 1) * vs);
+            ldg_cons<NV>(csrc + (long long)z * P, vs, u);
+        } else if (casrc) {
+            GCHK(casrc + (long long)(z - nb2) * P + (NV - 1) * vs);
+            ldg_cons<NV>(casrc + (long long)(z - nb2) * P, vs, u);
+        }
         else load_cons(ti, tj, z, u);
     };
 
@@ -410,12 +473,18 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 if (ZTOP) zrecon_top(kk + 1, w, zlo, zhn);
                 if (!PADRING) {
 #pragma unroll
-                    for (int v = 0; v < NV; v++) cur[v * CP + (tj + RO) * cw + ti + NG] = ring_at(kk, v);
+                    for (int v = 0; v < NV; v++) {
+                        SCHK(&cur[v * CP + (tj + RO) * cw + ti + NG]);
+                        cur[v * CP + (tj + RO) * cw + ti + NG] = ring_at(kk, v);
+                    }
                 }
             } else {
                 load_prim(ti, tj, kk, w);
 #pragma unroll
-                for (int v = 0; v < NV; v++) cur[v * CP + (tj + RO) * cw + ti + NG] = w[v];
+                for (int v = 0; v < NV; v++) {
+                    SCHK(&cur[v * CP + (tj + RO) * cw + ti + NG]);
+                    cur[v * CP + (tj + RO) * cw + ti + NG] = w[v];
+                }
             }
         }
         if (HLATE) {
@@ -426,7 +495,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 if (HSM) {
                     cp_async_wait_all();
 #pragma unroll
-                    for (int v = 0; v < NV; v++) hpre[v] = hs[v * nh + tid];
+                    for (int v = 0; v < NV; v++) {
+                        SCHK(hs + v * nh + tid);
+                        hpre[v] = hs[v * nh + tid];
+                    }
 #pragma unroll
                     for (int d = 0; d < NV - 2; d++)  // reflecting-boundary image: momentum sign
                         hpre[1 + d] = __hiloint2double(__double2hiint(hpre[1 + d]) ^ (((hzf >> (1 + d)) & 1) << 31),
@@ -435,7 +507,11 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                     if (kk + 1 < nb2) {
                         const double* src = hp + (long long)(kk + 1) * (hzf >> 4);
 #pragma unroll
-                        for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + tid, src + (long long)v * hvs);
+                        for (int v = 0; v < NV; v++) {
+                            SCHK(hs + v * nh + tid);
+                            GCHK(src + (long long)v * hvs);
+                            cp_async8(hs + v * nh + tid, src + (long long)v * hvs);
+                        }
                         cp_async_commit();
                     }
                 } else {
@@ -443,7 +519,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                     if (kk + 1 < nb2) load_halo(kk + 1, hpre);
                 }
 #pragma unroll
-                for (int v = 0; v < NV; v++) cur[v * CP + (hcy + RO) * cw + hcx + NG] = w[v];
+                for (int v = 0; v < NV; v++) {
+                    SCHK(&cur[v * CP + (hcy + RO) * cw + hcx + NG]);
+                    cur[v * CP + (hcy + RO) * cw + hcx + NG] = w[v];
+                }
             }
         } else {
             for (int h = tid; h < nh; h += blockDim.x) {
@@ -452,7 +531,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 double w[NV];
                 load_prim(cx, cy, kk, w);
 #pragma unroll
-                for (int v = 0; v < NV; v++) cur[v * CP + (cy + RO) * cw + cx + NG] = w[v];
+                for (int v = 0; v < NV; v++) {
+                    SCHK(&cur[v * CP + (cy + RO) * cw + cx + NG]);
+                    cur[v * CP + (cy + RO) * cw + cx + NG] = w[v];
+                }
             }
         }
         if (!ONEBAR) __syncthreads();
@@ -461,7 +543,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             double w[NV];
             cp_async_wait_all();  // no-op: complete since S4 of the previous plane
 #pragma unroll
-            for (int v = 0; v < NV; v++) hpre[v] = hs[v * nh + hid];
+            for (int v = 0; v < NV; v++) {
+                SCHK(hs + v * nh + hid);
+                hpre[v] = hs[v * nh + hid];
+            }
 #pragma unroll
             for (int d = 0; d < NV - 2; d++)  // reflecting-boundary image: momentum sign
                 hpre[1 + d] = __hiloint2double(__double2hiint(hpre[1 + d]) ^ (((hzf >> (1 + d)) & 1) << 31),
@@ -469,11 +554,18 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             ok &= cons_to_prim<NV>(hpre, w, gm1);
             double* nxt = ring + ((kk + 1 + NG) % RS_) * NV * CP + (hcy + RO) * cw + hcx + NG;
 #pragma unroll
-            for (int v = 0; v < NV; v++) nxt[v * CP] = w[v];
+            for (int v = 0; v < NV; v++) {
+                SCHK(nxt + v * CP);
+                nxt[v * CP] = w[v];
+            }
             if (kk + 2 < nb2) {
                 const double* src = hp + (long long)(kk + 2) * (hzf >> 4);
 #pragma unroll
-                for (int v = 0; v < NV; v++) cp_async8(hs + v * nh + hid, src + (long long)v * hvs);
+                for (int v = 0; v < NV; v++) {
+                        SCHK(hs + v * nh + hid);
+                        GCHK(src + (long long)v * hvs);
+                        cp_async8(hs + v * nh + hid, src + (long long)v * hvs);
+                    }
                 cp_async_commit();
             }
         }
@@ -491,6 +583,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             } else {
 #pragma unroll
                 for (int v = 0; v < NV; v++) {
+                    GCHK(up + v * vs + cidx);
+                    if (a != 0.0) GCHK(A.un + v * vs + cidx);
                     u0v[v] = __ldg(up + v * vs + cidx);
                     unv[v] = a != 0.0 ? __ldg(A.un + v * vs + cidx) : 0.0;
                 }
@@ -502,12 +596,20 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             for (int v = 0; v < NV; v++) {
                 double s[2 * R + 1], lo, hi;
                 const double* c = cur + v * CP + (tj + RO) * cw + ti + NG;
+                SCHK(c - R);
+                SCHK(c + R);
+                SCHK(XB + v * fxn + tj * fxs + ti);
+                SCHK(XA + v * fxn + tj * fxs + ti + 1);
 #pragma unroll
                 for (int m = 0; m <= 2 * R; m++) s[m] = c[m - R];
                 recon_cell<RECON>(s, lo, hi);
                 XB[v * fxn + tj * fxs + ti] = lo;
                 XA[v * fxn + tj * fxs + ti + 1] = hi;
                 if (NDIM >= 2) {
+                    SCHK(c - R * cw);
+                    SCHK(c + R * cw);
+                    SCHK(YB + v * fyn + tj * nb0 + ti);
+                    SCHK(YA + v * fyn + (tj + 1) * nb0 + ti);
 #pragma unroll
                     for (int m = 0; m <= 2 * R; m++) s[m] = c[(m - R) * cw];
                     recon_cell<RECON>(s, lo, hi);
@@ -527,18 +629,24 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             double s[2 * R + 1], lo, hi;
             if (xd) {
                 const double* c = cur + v * CP + (r + RO) * cw + (side ? nb0 : -1) + NG;
+                SCHK(c - R);
+                SCHK(c + R);
 #pragma unroll
                 for (int m = 0; m <= 2 * R; m++) s[m] = c[m - R];
             } else {
                 const double* c = cur + v * CP + ((side ? nb1 : -1) + RO) * cw + r + NG;
+                SCHK(c - R * cw);
+                SCHK(c + R * cw);
 #pragma unroll
                 for (int m = 0; m <= 2 * R; m++) s[m] = c[(m - R) * cw];
             }
             recon_cell<RECON>(s, lo, hi);
             if (xd) {
+                SCHK(side ? XB + v * fxn + r * fxs + nb0 : XA + v * fxn + r * fxs);
                 if (side) XB[v * fxn + r * fxs + nb0] = lo;
                 else XA[v * fxn + r * fxs] = hi;
             } else {
+                SCHK(side ? YB + v * fyn + nb1 * nb0 + r : YA + v * fyn + r);
                 if (side) YB[v * fyn + nb1 * nb0 + r] = lo;
                 else YA[v * fyn + r] = hi;
             }
@@ -559,8 +667,12 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             for (int v = 0; v < NV; v++) {
                 if (FC) {
                     const double* c = cur + v * CP + (r + RO) * cw + f + NG;  // cell f
+                    SCHK(c - (RECON ? 2 : 1));  // first order reads only the face's two cells
+                    SCHK(c + (RECON ? 1 : 0));
                     face_states<RECON>(c[-2], c[-1], c[0], c[1], wl[v], wr[v]);
                 } else {
+                    SCHK(XA + v * fxn + r * fxs + f);
+                    SCHK(XB + v * fxn + r * fxs + f);
                     wl[v] = XA[v * fxn + r * fxs + f];
                     wr[v] = XB[v * fxn + r * fxs + f];
                 }
@@ -575,7 +687,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             face_flux<NV, RS, 0>(wl, wr, shk_at(cur + (r + RO) * cw + f + NG, 1, 1), gamma, gm1i, fl);
             if (!ONEBAR) {  // ONEBAR: the own face stays in registers (shuffled in S4)
 #pragma unroll
-                for (int v = 0; v < NV; v++) XA[v * fxn + r * fxs + f] = fl[v];
+                for (int v = 0; v < NV; v++) {
+                    SCHK(XA + v * fxn + r * fxs + f);
+                    XA[v * fxn + r * fxs + f] = fl[v];
+                }
             }
         };
         auto yface = [&](int r, int f, double* fl) {
@@ -584,8 +699,12 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             for (int v = 0; v < NV; v++) {
                 if (FC) {
                     const double* c = cur + v * CP + (f + NG) * cw + r + NG;  // cell f of column r
+                    SCHK(c - (RECON ? 2 : 1) * cw);
+                    SCHK(c + (RECON ? 1 : 0) * cw);
                     face_states<RECON>(c[-2 * cw], c[-cw], c[0], c[cw], wl[v], wr[v]);
                 } else {
+                    SCHK(YA + v * fyn + f * nb0 + r);
+                    SCHK(YB + v * fyn + f * nb0 + r);
                     wl[v] = YA[v * fyn + f * nb0 + r];
                     wr[v] = YB[v * fyn + f * nb0 + r];
                 }
@@ -599,7 +718,10 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             }
             face_flux<NV, RS, 1>(wl, wr, shk_at(cur + (f + NG) * cw + r + NG, cw, 2), gamma, gm1i, fl);
 #pragma unroll
-            for (int v = 0; v < NV; v++) YA[v * fyn + f * nb0 + r] = fl[v];
+            for (int v = 0; v < NV; v++) {
+                SCHK(YA + v * fyn + f * nb0 + r);
+                YA[v * fyn + f * nb0 + r] = fl[v];
+            }
         };
         if (FUSE) {
             // 16x16 planes: the two independent solves of each round are issued
@@ -614,9 +736,15 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             for (int v = 0; v < NV; v++) {
                 if (FC) {  // x face ti+1 from cells ti-1..ti+2, y face tj+1 from tj-1..tj+2
                     const double* c = cur + v * CP + (tj + RO) * cw + ti + NG;
+                    SCHK(c - cw);
+                    SCHK(c + 2 * cw);
                     face_states<RECON>(c[-1], c[0], c[1], c[2], xl[v], xr[v]);
                     face_states<RECON>(c[-cw], c[0], c[cw], c[2 * cw], yl[v], yr[v]);
                 } else {
+                    SCHK(XA + v * fxn + xo);
+                    SCHK(XB + v * fxn + xo);
+                    SCHK(YA + v * fyn + yo);
+                    SCHK(YB + v * fyn + yo);
                     xl[v] = XA[v * fxn + xo];
                     xr[v] = XB[v * fxn + xo];
                     yl[v] = YA[v * fyn + yo];
@@ -644,6 +772,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             face_flux<NV, RS, 1>(yl, yr, shk_at(cur + (tj + 1 + NG) * cw + ti + NG, cw, 2), gamma, gm1i, fy);
 #pragma unroll
             for (int v = 0; v < NV; v++) {
+                SCHK(XA + v * fxn + xo);
+                SCHK(YA + v * fyn + yo);
                 XA[v * fxn + xo] = fx[v];
                 YA[v * fyn + yo] = fy[v];
             }
@@ -669,8 +799,12 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                     if (FC) {  // face 0 of row / column q from cells -2..1
                         const double* c = cur + v * CP + (isy ? NG * cw + q + NG : (q + RO) * cw + NG);
                         const int st = isy ? cw : 1;
+                        SCHK(c - (RECON ? 2 : 1) * st);
+                        SCHK(c + (RECON ? 1 : 0) * st);
                         face_states<RECON>(c[-2 * st], c[-st], c[0], c[st], bl[v], br[v]);
                     } else {
+                        SCHK(isy ? YA + v * fyn + q : XA + v * fxn + q * fxs);
+                        SCHK(isy ? YB + v * fyn + q : XB + v * fxn + q * fxs);
                         bl[v] = isy ? YA[v * fyn + q] : XA[v * fxn + q * fxs];
                         br[v] = isy ? YB[v * fyn + q] : XB[v * fxn + q * fxs];
                     }
@@ -698,6 +832,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 }
 #pragma unroll
                 for (int v = 0; v < NV; v++) {
+                    SCHK(isy ? YA + v * fyn + q : XA + v * fxn + q * fxs);
                     if (isy) YA[v * fyn + q] = fb[v];
                     else XA[v * fxn + q * fxs] = fb[v];
                 }
@@ -734,6 +869,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                         for (int v = 0; v < NV; v++) {
                             const double* c = cur + v * CP + (isy ? NG * cw + q + NG : (q + RO) * cw + NG);
                             const int st = isy ? cw : 1;
+                            SCHK(c - (RECON ? 2 : 1) * st);
+                            SCHK(c + (RECON ? 1 : 0) * st);
                             face_states<RECON>(c[-2 * st], c[-st], c[0], c[st], bl[v], br[v]);
                         }
                         if (!(positive(bl[0]) && positive(bl[NV - 1]) && positive(br[0]) && positive(br[NV - 1]))) {
@@ -758,6 +895,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                         }
 #pragma unroll
                         for (int v = 0; v < NV; v++) {
+                            SCHK(isy ? YA + v * fyn + q : XA + (ONEBAR ? v * nb1 + q : v * fxn + q * fxs));
                             if (isy) YA[v * fyn + q] = fb[v];
                             else XA[ONEBAR ? v * nb1 + q : v * fxn + q * fxs] = fb[v];
                         }
@@ -781,6 +919,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             double un[NV], Lv[NV];
 #pragma unroll
             for (int v = 0; v < NV; v++) {
+                if (!OWNF) SCHK(XA + v * fxn + tj * fxs + ti + 1);
+                SCHK(ONEBAR ? XA + v * nb1 + tj : XA + v * fxn + tj * fxs + ti);
                 const double fxp = OWNF ? fxo[v] : XA[v * fxn + tj * fxs + ti + 1];
                 double fxm;
                 if (ONEBAR) {  // left face: the left lane's own face, or the boundary face 0
@@ -793,6 +933,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 if (NDIM == 1) {
                     Lv[v] = -dfx;
                 } else {
+                    SCHK(YA + v * fyn + (tj + 1) * nb0 + ti);
+                    SCHK(YA + v * fyn + tj * nb0 + ti);
                     const double fyp = OWNF ? fyo[v] : YA[v * fyn + (tj + 1) * nb0 + ti];
                     const double dfy = (fyp - YA[v * fyn + tj * nb0 + ti]) * g.rdx[1];
                     if (NDIM == 2) Lv[v] = -(dfx + dfy);
@@ -802,6 +944,8 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
             if (L2PF) {
 #pragma unroll
                 for (int v = 0; v < NV; v++) {
+                    GCHK(up + v * vs + cidx);
+                    if (a != 0.0) GCHK(A.un + v * vs + cidx);
                     u0v[v] = __ldg(up + v * vs + cidx);
                     unv[v] = a != 0.0 ? __ldg(A.un + v * vs + cidx) : 0.0;
                 }
@@ -816,6 +960,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
                 const double u0 = u0v[v];
                 const double unn = unv[v];
                 const double uo = fma(bco, fma(dt, Lv[v], u0), a * unn);
+                GCHK(A.uout + v * vs + idx);
                 A.uout[v * vs + idx] = uo;
                 un[v] = uo;
                 fzlo[v] = fzhi[v];
