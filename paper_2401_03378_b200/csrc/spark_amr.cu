@@ -9,20 +9,22 @@
 // leaf list as the blocks).  All leaves advance with one dt (no subcycling).
 //
 // Per stage (lst:spark-nontelescoping body, with the coarse-fine guard rules):
-//   KA amr_interior / amr_guard  padded primitive tiles W[v][leaf][padded]:
-//        interior cells converted in place; face guards gathered through a
-//        host-built map (same-level copy, piecewise-constant prolongation,
+//   KA amr_fill_leaf  padded primitive tiles W[v][leaf][padded], one CTA per
+//        leaf: interior cells converted in place; face guards gathered through
+//        a host-built map (same-level copy, piecewise-constant prolongation,
 //        diagonal-pairwise restriction mean; reflect flips the momentum)
 //   KB amr_face    every face of every leaf: calcLims + calcFlux (the
 //        product's device reconstruction / Riemann / shockDet) -> F; the
 //        leaf-boundary faces also enter fluxBuff, B <- b_s (B + F)
 //   KC amr_update  updSoln: U^(s) = a U^n + b (U^(s-1) + dt L)
+//   KB+KC fused for 3-D 16^3 leaves and face-centric schemes (amr_leaf):
+//        KB1's plane march over the padded tiles, no face-flux array
 // Per step after the last stage: communicate_fluxes + correction (KD
 // amr_corr, one launch per direction so no two threads touch one cell),
 // then the CFL minimum of the corrected state (KE amr_cfl) for the next dt.
 //
-// This path is built for parity and measurement of the N3 row, not fused like
-// KB1: the padded tiles and the face fluxes go through HBM.
+// The padded tiles go through HBM (one write, one read per stage); the face
+// fluxes only on the unfused KB/KC path (other shapes and WENO).
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -74,27 +76,6 @@ __host__ __device__ inline long long face_cell(const AmrGeo& g, int d, int i, in
 }
 
 // ---------------------------------------------------------------- KA
-template <int NV>
-__global__ void amr_interior_kernel(const AmrGeo g, const double* __restrict__ u, double* __restrict__ w,
-                                    int to_prim, DevScalars* sc) {
-    const long long vs = g.nleaf * g.nc, vp = g.nleaf * g.np;
-    const int gx = g.ng, gy = g.ndim >= 2 ? g.ng : 0, gz = g.ndim >= 3 ? g.ng : 0;
-    bool ok = true;
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < vs;
-         q += (long long)gridDim.x * blockDim.x) {
-        const long long leaf = q / g.nc, c = q - leaf * g.nc;
-        const int i = (int)(c % g.nb[0]), j = (int)((c / g.nb[0]) % g.nb[1]), k = (int)(c / ((long long)g.nb[0] * g.nb[1]));
-        const long long p = leaf * g.np + ((long long)(k + gz) * g.pn[1] + (j + gy)) * g.pn[0] + (i + gx);
-        double uu[NV], ww[NV];
-#pragma unroll
-        for (int v = 0; v < NV; v++) uu[v] = u[v * vs + q];
-        if (to_prim) ok &= cons_to_prim<NV>(uu, ww, g.gamma - 1.0);
-#pragma unroll
-        for (int v = 0; v < NV; v++) w[v * vp + p] = to_prim ? ww[v] : uu[v];
-    }
-    if (!ok) flag_nonphysical(sc);
-}
-
 // conserved value v of a guard source: copy, or the restriction mean of the
 // 2^ndim fine children (diagonal pairs, reading R22)
 template <int NV>
@@ -107,14 +88,36 @@ __device__ __forceinline__ double guard_value(const AmrGeo& g, const double* __r
            0.125;
 }
 
+// KA in one launch, one CTA per leaf: its interior cells, then its guard
+// entries (the map lists them leaf by leaf; goff[leaf] is the first).  The
+// guard sources are neighbour leaves' interiors, read while they are still in
+// L2 from the neighbouring CTAs' interior pass (the leaf order follows the
+// block grid).
 template <int NV>
-__global__ void amr_guard_kernel(const AmrGeo g, const double* __restrict__ u, const GuardE* __restrict__ ge,
-                                 long long n, const double* __restrict__ grecv, double* __restrict__ w, int to_prim,
-                                 DevScalars* sc) {
+__global__ void __launch_bounds__(256) amr_fill_leaf_kernel(const AmrGeo g, const double* __restrict__ u,
+                                                            const GuardE* __restrict__ ge,
+                                                            const long long* __restrict__ goff,
+                                                            const double* __restrict__ grecv, double* __restrict__ w,
+                                                            int to_prim, DevScalars* sc) {
     const long long vs = g.nleaf * g.nc, vp = g.nleaf * g.np;
+    const int gx = g.ng, gy = g.ndim >= 2 ? g.ng : 0, gz = g.ndim >= 3 ? g.ng : 0;
+    const long long leaf = blockIdx.x;
     bool ok = true;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
-         e += (long long)gridDim.x * blockDim.x) {
+#pragma unroll 4
+    for (long long c = threadIdx.x; c < g.nc; c += blockDim.x) {
+        const long long q = leaf * g.nc + c;
+        const int i = (int)(c % g.nb[0]), j = (int)((c / g.nb[0]) % g.nb[1]), k = (int)(c / ((long long)g.nb[0] * g.nb[1]));
+        const long long p = leaf * g.np + ((long long)(k + gz) * g.pn[1] + (j + gy)) * g.pn[0] + (i + gx);
+        double uu[NV], ww[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) uu[v] = u[v * vs + q];
+        if (to_prim) ok &= cons_to_prim<NV>(uu, ww, g.gamma - 1.0);
+#pragma unroll
+        for (int v = 0; v < NV; v++) w[v * vp + p] = to_prim ? ww[v] : uu[v];
+    }
+    const long long e1 = goff[leaf + 1];
+#pragma unroll 4
+    for (long long e = goff[leaf] + threadIdx.x; e < e1; e += blockDim.x) {
         const GuardE E = ge[e];
         double uu[NV], ww[NV];
 #pragma unroll
@@ -270,6 +273,227 @@ __global__ void amr_update_kernel(const AmrGeo g, const double* __restrict__ F, 
             const double unn = a != 0.0 ? un[v * vs + q] : 0.0;
             uout[v * vs + q] = fma(b, fma(dt, Lv, u0), a * unn);
         }
+    }
+}
+
+// ------------------------------------------------------- KB+KC fused (3-D)
+// 16^3 leaves, face-centric schemes (first order, PLM, PLM-MC): one CTA per
+// leaf marches its 16 planes like KB1 (one thread per column).  The padded
+// primitive planes of the tile W that KA filled (guards included, so no
+// gathering) stream into a 5-slot shared-memory ring (planes k-1 .. k+3, each
+// copied by 16-byte cp.async four planes ahead of its first use), and each
+// face is solved once: the own +x / +y / +z faces, on warp 0 the 32 faces at
+// x = 0 and y = 0 of the plane (y faces in the x frame with u_x <-> u_y
+// swapped, bitwise identical), the z face below the first plane in the
+// prologue.  -x fluxes come from the left lane (shuffle), -y fluxes from the
+// row below through shared memory (double-buffered by plane parity: one
+// barrier per plane), -z from the previous plane (register).  The update and
+// the fluxBuff accumulation of the leaf's six faces follow in the same pass,
+// so KB's face-flux array never exists.  Same face arithmetic as KB
+// (reconstruction, positivity fallback, shockDet, Riemann).
+constexpr int kLeafN = 16, kLeafSlots = 5;
+
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int RECON, int RS>
+__global__ void __launch_bounds__(256, 2)
+    amr_leaf_kernel(const AmrGeo g, const double* __restrict__ w, const double* __restrict__ uprev,
+                    const double* __restrict__ un, double* __restrict__ uout, double* __restrict__ B, double a,
+                    double bco, const DevScalars* __restrict__ sc) {
+    constexpr int NV = 5, N = kLeafN, NS = kLeafSlots;
+    extern __shared__ double smem[];
+    const int pn0 = g.pn[0], gd = g.ng;
+    const int PL = pn0 * g.pn[1];  // cells of a padded plane (even: pn = 16 + 2 ng)
+    double* const ring = smem;                  // [NS][NV][PL]
+    double* const XA = ring + NS * NV * PL;     // [2][NV][N]: x face 0 of each row
+    double* const YA = XA + 2 * NV * N;         // [2][NV][(N + 1) N]: y faces [row face][column]
+    // fluxBuff values of the plane's x / y leaf faces (slots 0-3), staged by
+    // cp.async a plane ahead: [2][4][NV][N] (the read-modify-write of B would
+    // otherwise wait on HBM in every plane)
+    double* const BS = YA + 2 * NV * (N + 1) * N;
+    const long long leaf = blockIdx.x;
+    const int tid = threadIdx.x, ti = tid % N, tj = tid / N;
+    const int lev = leaf < g.ncl ? 0 : 1;
+    const double r0 = g.rdx[lev][0], r1 = g.rdx[lev][1], r2 = g.rdx[lev][2];
+    const double dt = sc->dt, gamma = g.gamma, gm1i = 1.0 / (g.gamma - 1.0);
+    const bool active = sc->active != 0;
+    const long long vp = g.nleaf * g.np, vs = g.nleaf * g.nc, bvs = g.nleaf * 6 * g.mf;
+    const double* const Wl = w + leaf * g.np;
+    auto plane = [&](int z) { return ring + ((z + 2 * NS) % NS) * NV * PL; };
+    auto load_plane = [&](int z) {  // padded plane z (all variables) into its slot
+        double* dst = plane(z);
+        const double* src = Wl + (long long)(z + gd) * PL;
+        const int half = PL / 2;
+        for (int e = tid; e < NV * half; e += blockDim.x) {
+            const int v = e / half, c = e - v * half;
+            cp_async16(dst + v * PL + 2 * c, src + v * vp + 2 * c);
+        }
+    };
+    auto stage_b = [&](int z) {  // fluxBuff of plane z's x / y leaf faces -> BS[z & 1]
+        double* dst = BS + (z & 1) * 4 * NV * N;
+        for (int e = tid; e < 4 * NV * (N / 2); e += blockDim.x) {
+            const int sv = e / (N / 2), c = e - sv * (N / 2);  // sv = slot * NV + v
+            const int slot = sv / NV, v = sv - slot * NV;
+            cp_async16(dst + sv * N + 2 * c, B + v * bvs + (leaf * 6 + slot) * g.mf + (long long)z * N + 2 * c);
+        }
+    };
+    auto commit = [] { asm volatile("cp.async.commit_group;\n" ::: "memory"); };
+    const int own = (tj + gd) * pn0 + ti + gd;  // this column's cell in a padded plane
+    // Riemann flux from the two states (+ shock flag); D 0 / 1 (x frame) / 2
+    auto finish = [&](double* wl, double* wr, bool shk, int D, bool swapxy, double* f) {
+        if (D == 2) {
+            face_flux<NV, RS, 2>(wl, wr, shk, gamma, gm1i, f);
+        } else {
+            if (swapxy) {  // a y face solved in the x frame
+                double t = wl[1]; wl[1] = wl[2]; wl[2] = t;
+                t = wr[1]; wr[1] = wr[2]; wr[2] = t;
+            }
+            face_flux<NV, RS, 0>(wl, wr, shk, gamma, gm1i, f);
+            if (swapxy) {
+                const double t = f[1];
+                f[1] = f[2];
+                f[2] = t;
+            }
+        }
+    };
+    // face between the cells q[1] and q[2] of a line q[0..3] (variable 0; the
+    // other variables PL further), normal variable 1 + D
+    auto solve = [&](const double* const* q, int D, bool swapxy, double* f) {
+        double wl[NV], wr[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) {
+            if (RECON == 0) {
+                wl[v] = q[1][v * PL];
+                wr[v] = q[2][v * PL];
+            } else {
+                face_states<RECON>(q[0][v * PL], q[1][v * PL], q[2][v * PL], q[3][v * PL], wl[v], wr[v]);
+            }
+        }
+        if (RECON != 0 && !(positive(wl[0]) && positive(wl[NV - 1]) && positive(wr[0]) && positive(wr[NV - 1]))) {
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                wl[v] = q[1][v * PL];
+                wr[v] = q[2][v * PL];
+            }
+        }
+        bool shk = false;
+        if constexpr (RS == 2) {
+            double uu[4], pp[4], rr[4];
+#pragma unroll
+            for (int m = 0; m < 4; m++) {
+                uu[m] = q[m][(1 + D) * PL];
+                pp[m] = q[m][(NV - 1) * PL];
+                rr[m] = q[m][0];
+            }
+            shk = shock_face(uu, pp, rr, g.shock_thresh, gamma);
+        }
+        finish(wl, wr, shk, D, swapxy, f);
+    };
+    auto line = [&](const double* c, int st, const double** q) {  // cells c-2st .. c+st
+        q[0] = c - 2 * st;
+        q[1] = c - st;
+        q[2] = c;
+        q[3] = c + st;
+    };
+    auto zline = [&](int z, const double** q) {  // this column, planes z-2 .. z+1
+        for (int m = 0; m < 4; m++) q[m] = plane(z - 2 + m) + own;
+    };
+    auto fbuf = [&](int slot, long long cell, const double* f) {  // fluxBuff, reading R23
+        const long long bi = (leaf * 6 + slot) * g.mf + cell;
+#pragma unroll
+        for (int v = 0; v < NV; v++) B[v * bvs + bi] = bco * (B[v * bvs + bi] + f[v]);
+    };
+    // the same for the x / y leaf faces of plane z from the staged values
+    auto fbuf_s = [&](int z, int slot, int i, const double* f) {
+        const double* bs = BS + (z & 1) * 4 * NV * N + slot * NV * N + i;
+        const long long bi = (leaf * 6 + slot) * g.mf + (long long)z * N + i;
+#pragma unroll
+        for (int v = 0; v < NV; v++) B[v * bvs + bi] = bco * (bs[v * N] + f[v]);
+    };
+
+    // prologue: planes -2 .. 2, the z face below plane 0, then plane 3 into
+    // plane -2's slot
+    for (int z = -2; z <= 2; z++) load_plane(z);
+    stage_b(0);
+    commit();
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    double fzlo[NV], fzhi[NV];
+    {
+        const double* q[4];
+        zline(0, q);
+        solve(q, 2, false, fzlo);
+    }
+    fbuf(4, (long long)tj * N + ti, fzlo);
+    __syncthreads();  // plane -2 read by every thread
+    load_plane(3);
+    commit();
+    // (an L2 prefetch of the S4 operands one or two planes ahead measured
+    // slower: 6.42 -> 5.98 G zone-updates/s)
+    for (int kk = 0; kk < N; kk++) {
+        const int pb = kk & 1;
+        double* const XK = XA + pb * NV * N;
+        double* const YK = YA + pb * NV * (N + 1) * N;
+        const double* const cur = plane(kk);
+        // ---------------------------------------------------------- S3
+        double fx[NV];
+        {
+            const double* q[4];
+            line(cur + own + 1, 1, q);
+            solve(q, 0, false, fx);
+            double fy[NV];
+            line(cur + own + pn0, pn0, q);
+            solve(q, 1, true, fy);
+#pragma unroll
+            for (int v = 0; v < NV; v++) YK[v * (N + 1) * N + (tj + 1) * N + ti] = fy[v];
+            zline(kk + 1, q);
+            solve(q, 2, false, fzhi);
+        }
+        if (tid < 32) {  // warp 0: x face 0 of row q (lanes 0-15), y face 0 of column q (16-31)
+            const bool isy = tid >= 16;
+            const int r = tid & 15;
+            const double* q[4];
+            if (isy) line(cur + gd * pn0 + r + gd, pn0, q);
+            else line(cur + (r + gd) * pn0 + gd, 1, q);
+            double fb[NV];
+            solve(q, isy ? 1 : 0, isy, fb);
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                if (isy) YK[v * (N + 1) * N + r] = fb[v];
+                else XK[v * N + r] = fb[v];
+            }
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // plane kk+3 (issued a plane ago) landed
+        __syncthreads();
+        // ---------------------------------------------------------- S4
+        // plane kk+4 into plane kk-1's slot (read by S3 of plane kk only) and the
+        // fluxBuff values of plane kk+1 (BS[(kk+1) & 1], last read in S4(kk-1))
+        if (kk + 4 < N + 2) load_plane(kk + 4);
+        if (kk + 1 < N) stage_b(kk + 1);
+        commit();
+        double fxm[NV], fym[NV], fyp[NV];
+        const long long cidx = leaf * g.nc + ((long long)kk * N + tj) * N + ti;
+#pragma unroll
+        for (int v = 0; v < NV; v++) {
+            const double nbr = __shfl_up_sync(0xffffffffu, fx[v], 1);
+            fxm[v] = ti == 0 ? XK[v * N + tj] : nbr;
+            fym[v] = YK[v * (N + 1) * N + tj * N + ti];
+            fyp[v] = YK[v * (N + 1) * N + (tj + 1) * N + ti];
+            const double Lv = -((fx[v] - fxm[v]) * r0 + (fyp[v] - fym[v]) * r1) - (fzhi[v] - fzlo[v]) * r2;
+            const double u0 = uprev[v * vs + cidx];
+            const double unn = a != 0.0 ? un[v * vs + cidx] : 0.0;
+            uout[v * vs + cidx] = active ? fma(bco, fma(dt, Lv, u0), a * unn) : u0;
+        }
+        if (ti == 0) fbuf_s(kk, 0, tj, fxm);
+        if (ti == N - 1) fbuf_s(kk, 1, tj, fx);
+        if (tj == 0) fbuf_s(kk, 2, ti, fym);
+        if (tj == N - 1) fbuf_s(kk, 3, ti, fyp);
+        if (kk == N - 1) fbuf(5, (long long)tj * N + ti, fzhi);
+#pragma unroll
+        for (int v = 0; v < NV; v++) fzlo[v] = fzhi[v];
     }
 }
 
@@ -672,7 +896,24 @@ struct RankPlan {
     std::vector<long long> gsend_off, grecv_off;  // per peer rank, size nranks + 1
     std::vector<long long> fsend;               // local B index (variable 0) of each value sent
     std::vector<long long> fsend_off, frecv_off;
+    std::vector<long long> goff;                // first guard entry of each local leaf, size nleaf + 1
 };
+
+// KB+KC fused (3-D 16^3 leaves, face-centric schemes): no face-flux array
+bool leaf_fused(const AmrGeo& g) {
+    return g.ndim == 3 && g.nb[0] == spark::kLeafN && g.nb[1] == spark::kLeafN && g.nb[2] == spark::kLeafN &&
+           (g.recon == 0 || g.recon == 1 || g.recon == 3);
+}
+
+// per-leaf offsets of a guard list ordered by leaf (dst = leaf * np + ...)
+std::vector<long long> guard_offsets(const std::vector<GuardE>& gs, long long nleaf, long long np) {
+    std::vector<long long> off(nleaf + 1, 0);
+    for (const GuardE& e : gs) off[e.dst / np + 1]++;
+    for (long long l = 0; l < nleaf; l++) off[l + 1] += off[l];
+    for (size_t i = 1; i < gs.size(); i++)
+        if (gs[i].dst / np < gs[i - 1].dst / np) throw AmrError(SPARK_ERR_STATE, "guard map not ordered by leaf");
+    return off;
+}
 
 std::vector<RankPlan> partition(const AmrPlan& P, int nranks) {
     const AmrGeo& G = P.g;
@@ -767,7 +1008,8 @@ size_t rank_bytes(const RankPlan& p) {
     size_t b = al(sizeof(spark::DevScalars));
     b += 3 * al(sizeof(double) * g.nv * g.nleaf * g.nc);       // U^n and two stage buffers
     b += al(sizeof(double) * g.nv * g.nleaf * g.np);            // padded tiles
-    b += al(sizeof(double) * g.nv * g.nleaf * g.NF);            // face fluxes
+    if (!leaf_fused(g)) b += al(sizeof(double) * g.nv * g.nleaf * g.NF);  // face fluxes (unfused KB/KC)
+    b += al(sizeof(long long) * (g.nleaf + 1));                 // guard offsets per leaf
     b += al(sizeof(double) * g.nv * g.nleaf * 6 * g.mf);        // fluxBuff
     b += al(sizeof(GuardE) * std::max<size_t>(1, p.guards.size()));
     for (int d = 0; d < 3; d++) b += al(sizeof(CorrE) * std::max<size_t>(1, p.corr[d].size()));
@@ -797,6 +1039,7 @@ struct spark_amr {
     CorrE* corr[3] = {};
     GuardE* gitems = nullptr;
     long long* fitems = nullptr;
+    long long* goff = nullptr;  // first guard entry of each leaf
     double *gsend = nullptr, *grecv = nullptr, *fsend = nullptr, *frecv = nullptr;
     int n_idx = 0;
     bool have_state = false;
@@ -827,18 +1070,14 @@ void launched(cudaError_t e, const char* what) {
 // padded tiles of state u: interior + face guards; primitives (to_prim) or conserved
 void amr_fill(spark_amr* a, const double* u, double* w, int to_prim) {
     const AmrGeo& g = a->rp.g;
-    const long long nG = (long long)a->rp.guards.size();
-    const unsigned gi = spark::grid_of(g.nleaf * g.nc), gg = spark::grid_of(nG);
-    if (g.ndim == 1) {
-        spark::amr_interior_kernel<3><<<gi, 256, 0, a->stream>>>(g, u, w, to_prim, a->sc);
-        if (nG) spark::amr_guard_kernel<3><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, a->grecv, w, to_prim, a->sc);
-    } else if (g.ndim == 2) {
-        spark::amr_interior_kernel<4><<<gi, 256, 0, a->stream>>>(g, u, w, to_prim, a->sc);
-        if (nG) spark::amr_guard_kernel<4><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, a->grecv, w, to_prim, a->sc);
-    } else {
-        spark::amr_interior_kernel<5><<<gi, 256, 0, a->stream>>>(g, u, w, to_prim, a->sc);
-        if (nG) spark::amr_guard_kernel<5><<<gg, 256, 0, a->stream>>>(g, u, a->guards, nG, a->grecv, w, to_prim, a->sc);
-    }
+    if (g.nleaf == 0) return;
+    const unsigned nb = (unsigned)g.nleaf;
+    if (g.ndim == 1)
+        spark::amr_fill_leaf_kernel<3><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim, a->sc);
+    else if (g.ndim == 2)
+        spark::amr_fill_leaf_kernel<4><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim, a->sc);
+    else
+        spark::amr_fill_leaf_kernel<5><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim, a->sc);
     launched(cudaGetLastError(), "amr fill");
 }
 
@@ -853,10 +1092,37 @@ void faces_d(spark_amr* a, double bco) {
     launched(cudaGetLastError(), "amr faces");
 }
 
+template <int RECON, int RS>
+void leaf_t(spark_amr* a, const double* prev, const double* un, double sa, double sb, double* out) {
+    const AmrGeo& g = a->rp.g;
+    const size_t smem = sizeof(double) * ((size_t)spark::kLeafSlots * g.nv * g.pn[0] * g.pn[1] +
+                                          2 * (size_t)g.nv * spark::kLeafN +
+                                          2 * (size_t)g.nv * (spark::kLeafN + 1) * spark::kLeafN +
+                                          2 * 4 * (size_t)g.nv * spark::kLeafN);
+    auto k = spark::amr_leaf_kernel<RECON, RS>;
+    launched(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "amr leaf smem");
+    k<<<(unsigned)g.nleaf, 256, smem, a->stream>>>(g, a->W, prev, un, out, a->B, sa, sb, a->sc);
+}
+
+template <int RECON>
+void leaf_r(spark_amr* a, int rs, const double* prev, const double* un, double sa, double sb, double* out) {
+    if (rs == 0) leaf_t<RECON, 0>(a, prev, un, sa, sb, out);
+    else if (rs == 1 || RECON == 0) leaf_t<RECON, 1>(a, prev, un, sa, sb, out);
+    else leaf_t<RECON, 2>(a, prev, un, sa, sb, out);
+}
+
 void amr_stage(spark_amr* a, const double* prev, const double* un, double sa, double sb, double* out) {
     const AmrGeo& g = a->rp.g;
     if (g.nleaf == 0) return;
     amr_fill(a, prev, a->W, 1);
+    if (leaf_fused(g)) {
+        const int rs = a->plan.c.riemann;
+        if (g.recon == 0) leaf_r<0>(a, rs, prev, un, sa, sb, out);
+        else if (g.recon == 1) leaf_r<1>(a, rs, prev, un, sa, sb, out);
+        else leaf_r<3>(a, rs, prev, un, sa, sb, out);
+        launched(cudaGetLastError(), "amr leaf stage");
+        return;
+    }
     if (g.ndim == 1) faces_d<1>(a, sb);
     else if (g.ndim == 2) faces_d<2>(a, sb);
     else faces_d<3>(a, sb);
@@ -955,7 +1221,8 @@ void carve_member(spark_amr* a, void* arena, size_t arena_bytes) {
     a->sc = reinterpret_cast<spark::DevScalars*>(take(sizeof(spark::DevScalars)));
     for (int i = 0; i < 3; i++) a->U[i] = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * g.nc));
     a->W = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * g.np));
-    a->F = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * g.NF));
+    if (!leaf_fused(g)) a->F = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * g.NF));
+    a->goff = reinterpret_cast<long long*>(take(sizeof(long long) * (g.nleaf + 1)));
     a->B = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * 6 * g.mf));
     a->guards = reinterpret_cast<GuardE*>(take(sizeof(GuardE) * std::max<size_t>(1, rp.guards.size())));
     for (int d = 0; d < 3; d++)
@@ -971,6 +1238,8 @@ void carve_member(spark_amr* a, void* arena, size_t arena_bytes) {
         if (bytes) ACU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, a->stream));
     };
     up(a->guards, rp.guards.data(), sizeof(GuardE) * rp.guards.size());
+    const std::vector<long long> goff = guard_offsets(rp.guards, g.nleaf, g.np);
+    up(a->goff, goff.data(), sizeof(long long) * goff.size());
     for (int d = 0; d < 3; d++) up(a->corr[d], rp.corr[d].data(), sizeof(CorrE) * rp.corr[d].size());
     up(a->gitems, rp.gsend.data(), sizeof(GuardE) * ngs);
     up(a->fitems, rp.fsend.data(), sizeof(long long) * nfs);

@@ -49,6 +49,12 @@ CASES = [
     (P("2d_hybrid", 2, (8, 8, 1), (4, 4, 1), 2, 1, 2, 2, 0.4, ((1, 1), (1, 1), (1, 1)), 0.5), (1, 1, 0), (3, 3, 1)),
     (P("3d_plm", 3, (8, 8, 8), (3, 3, 3), 2, 1, 1, 2, 0.3, ((0, 0), (1, 2), (2, 1))), (1, 1, 1), (2, 2, 2)),
     (P("3d_weno", 3, (6, 6, 6), (2, 3, 2), 3, 2, 1, 3, 0.3, ((0, 0), (0, 0), (0, 0))), (0, 1, 0), (1, 2, 2)),
+    # 16^3 leaves: the fused leaf kernel (face-centric schemes), every BC kind
+    (P("3d_plm16", 3, (16, 16, 16), (3, 3, 3), 2, 1, 1, 2, 0.3, ((0, 0), (1, 2), (2, 1))), (1, 1, 1), (2, 2, 2)),
+    (P("3d_mc16_hll", 3, (16, 16, 16), (2, 3, 2), 2, 3, 0, 3, 0.3, ((2, 2), (0, 0), (1, 1))), (0, 1, 0), (1, 2, 2)),
+    (P("3d_first16", 3, (16, 16, 16), (3, 2, 2), 2, 0, 1, 2, 0.3, ((1, 1), (2, 2), (0, 0))), (1, 0, 1), (3, 1, 2)),
+    (P("3d_hybrid16", 3, (16, 16, 16), (2, 2, 3), 2, 1, 2, 2, 0.3, ((0, 0), (0, 0), (2, 2)), 0.5), (0, 0, 1),
+     (2, 1, 2)),
 ]
 
 
@@ -139,7 +145,7 @@ def test_failure_rolls_back(sp):
 
 
 @pytest.mark.parametrize("nranks", [2, 3, 5])
-@pytest.mark.parametrize("p,rlo,rhi", [CASES[2], CASES[5], CASES[6], CASES[7]],
+@pytest.mark.parametrize("p,rlo,rhi", [CASES[2], CASES[5], CASES[6], CASES[7], CASES[8], CASES[11]],
                          ids=lambda x: getattr(x, "name", str(x)))
 def test_virtual_ranks_bitwise(sp, p, rlo, rhi, nranks):
     """The leaf list split into nranks contiguous ranges: guard values and the

@@ -61,7 +61,8 @@ def main():
     ci = {h: i for i, h in enumerate(hdr)}
     # template args "<(int)3, (int)1, (int)1, (int)16, (int)16>" -> mangled "ILi3ELi1ELi1ELi16ELi16E"
     targs = re.findall(r"\(int\)(\d+)", b["name"])
-    fn, lm = line_map(cubin, ["stage_kernel", "I" + "".join(f"Li{a}E" for a in targs)])
+    kname = re.search(r"::(\w+)<", b["name"]).group(1)  # e.g. stage_kernel, amr_leaf_kernel
+    fn, lm = line_map(cubin, [kname, "I" + "".join(f"Li{a}E" for a in targs)])
     samples = collections.Counter()
     stall = collections.defaultdict(collections.Counter)
     execd = collections.Counter()
