@@ -98,13 +98,13 @@ __global__ void __launch_bounds__(256) amr_fill_leaf_kernel(const AmrGeo g, cons
                                                             const GuardE* __restrict__ ge,
                                                             const long long* __restrict__ goff,
                                                             const double* __restrict__ grecv, double* __restrict__ w,
-                                                            int to_prim, DevScalars* sc) {
+                                                            int to_prim, int interior, DevScalars* sc) {
     const long long vs = g.nleaf * g.nc, vp = g.nleaf * g.np;
     const int gx = g.ng, gy = g.ndim >= 2 ? g.ng : 0, gz = g.ndim >= 3 ? g.ng : 0;
     const long long leaf = blockIdx.x;
     bool ok = true;
 #pragma unroll 4
-    for (long long c = threadIdx.x; c < g.nc; c += blockDim.x) {
+    for (long long c = threadIdx.x; interior && c < g.nc; c += blockDim.x) {
         const long long q = leaf * g.nc + c;
         const int i = (int)(c % g.nb[0]), j = (int)((c / g.nb[0]) % g.nb[1]), k = (int)(c / ((long long)g.nb[0] * g.nb[1]));
         const long long p = leaf * g.np + ((long long)(k + gz) * g.pn[1] + (j + gy)) * g.pn[0] + (i + gx);
@@ -291,7 +291,7 @@ __global__ void amr_update_kernel(const AmrGeo g, const double* __restrict__ F, 
 // the fluxBuff accumulation of the leaf's six faces follow in the same pass,
 // so KB's face-flux array never exists.  Same face arithmetic as KB
 // (reconstruction, positivity fallback, shockDet, Riemann).
-constexpr int kLeafN = 16, kLeafSlots = 5;
+constexpr int kLeafN = 16, kLeafSlots = 5, kLeafNG = 2;
 
 __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -302,11 +302,11 @@ template <int RECON, int RS>
 __global__ void __launch_bounds__(256, 2)
     amr_leaf_kernel(const AmrGeo g, const double* __restrict__ w, const double* __restrict__ uprev,
                     const double* __restrict__ un, double* __restrict__ uout, double* __restrict__ B, double a,
-                    double bco, const DevScalars* __restrict__ sc) {
+                    double bco, DevScalars* __restrict__ sc) {
     constexpr int NV = 5, N = kLeafN, NS = kLeafSlots;
     extern __shared__ double smem[];
-    const int pn0 = g.pn[0], gd = g.ng;
-    const int PL = pn0 * g.pn[1];  // cells of a padded plane (even: pn = 16 + 2 ng)
+    constexpr int gd = kLeafNG, pn0 = N + 2 * gd;  // the tile's guard depth (leaf_fused)
+    constexpr int PL = pn0 * pn0;                   // cells of a padded plane
     double* const ring = smem;                  // [NS][NV][PL]
     double* const XA = ring + NS * NV * PL;     // [2][NV][N]: x face 0 of each row
     double* const YA = XA + 2 * NV * N;         // [2][NV][(N + 1) N]: y faces [row face][column]
@@ -323,14 +323,52 @@ __global__ void __launch_bounds__(256, 2)
     const long long vp = g.nleaf * g.np, vs = g.nleaf * g.nc, bvs = g.nleaf * 6 * g.mf;
     const double* const Wl = w + leaf * g.np;
     auto plane = [&](int z) { return ring + ((z + 2 * NS) % NS) * NV * PL; };
-    auto load_plane = [&](int z) {  // padded plane z (all variables) into its slot
+    const int own = (tj + gd) * pn0 + ti + gd;  // this column's cell in a padded plane
+    // padded plane z (all variables) into its slot: a guard plane (z < 0 or
+    // z >= N) whole from W; an interior plane's N x N interior as CONSERVED
+    // values straight from U^(s-1) (converted in place by each column's
+    // thread, convert() below; KA then writes no interior) and its guard
+    // frame from W.  16-byte copies (gd even: every row piece is aligned).
+    auto load_plane = [&](int z) {
         double* dst = plane(z);
         const double* src = Wl + (long long)(z + gd) * PL;
-        const int half = PL / 2;
-        for (int e = tid; e < NV * half; e += blockDim.x) {
-            const int v = e / half, c = e - v * half;
-            cp_async16(dst + v * PL + 2 * c, src + v * vp + 2 * c);
+        if (z < 0 || z >= N) {
+            const int half = PL / 2;
+            for (int e = tid; e < NV * half; e += blockDim.x) {
+                const int v = e / half, c = e - v * half;
+                cp_async16(dst + v * PL + 2 * c, src + v * vp + 2 * c);
+            }
+            return;
         }
+        const int nint = N * N / 2, nrow = gd * pn0, per = nint + nrow + N * gd;  // 16-byte pieces per variable
+        const double* uz = uprev + leaf * g.nc + (long long)z * N * N;
+        for (int e = tid; e < NV * per; e += blockDim.x) {
+            const int v = e / per;
+            int c = e - v * per;
+            if (c < nint) {  // interior row r, pieces of 2
+                const int r = c / (N / 2), x = 2 * (c - r * (N / 2));
+                cp_async16(dst + v * PL + (r + gd) * pn0 + gd + x, uz + v * vs + r * N + x);
+            } else if ((c -= nint) < nrow) {  // the gd rows below and above the interior
+                const int rr = c / (pn0 / 2), x = 2 * (c - rr * (pn0 / 2));
+                const int y = rr < gd ? rr : rr + N;  // padded row
+                cp_async16(dst + v * PL + y * pn0 + x, src + v * vp + y * pn0 + x);
+            } else {  // left / right guard columns of the interior rows
+                c -= nrow;
+                const int r = c / gd, k = c - r * gd;  // k < gd / 2: left, else right
+                const int x = k < gd / 2 ? 2 * k : gd + N + 2 * (k - gd / 2);
+                cp_async16(dst + v * PL + (r + gd) * pn0 + x, src + v * vp + (r + gd) * pn0 + x);
+            }
+        }
+    };
+    bool ok = true;
+    auto convert = [&](int z) {  // this column's cell of interior plane z: conserved -> primitive
+        double* c = plane(z) + own;
+        double u[NV], wv[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) u[v] = c[v * PL];
+        ok &= cons_to_prim<NV>(u, wv, g.gamma - 1.0);
+#pragma unroll
+        for (int v = 0; v < NV; v++) c[v * PL] = wv[v];
     };
     auto stage_b = [&](int z) {  // fluxBuff of plane z's x / y leaf faces -> BS[z & 1]
         double* dst = BS + (z & 1) * 4 * NV * N;
@@ -341,7 +379,6 @@ __global__ void __launch_bounds__(256, 2)
         }
     };
     auto commit = [] { asm volatile("cp.async.commit_group;\n" ::: "memory"); };
-    const int own = (tj + gd) * pn0 + ti + gd;  // this column's cell in a padded plane
     // Riemann flux from the two states (+ shock flag); D 0 / 1 (x frame) / 2
     auto finish = [&](double* wl, double* wr, bool shk, int D, bool swapxy, double* f) {
         if (D == 2) {
@@ -421,6 +458,7 @@ __global__ void __launch_bounds__(256, 2)
     commit();
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
+    for (int z = 0; z <= 2; z++) convert(z);  // own cells: read by this thread first, by others after the next barrier
     double fzlo[NV], fzhi[NV];
     {
         const double* q[4];
@@ -471,6 +509,7 @@ __global__ void __launch_bounds__(256, 2)
         // ---------------------------------------------------------- S4
         // plane kk+4 into plane kk-1's slot (read by S3 of plane kk only) and the
         // fluxBuff values of plane kk+1 (BS[(kk+1) & 1], last read in S4(kk-1))
+        if (kk + 3 < N) convert(kk + 3);  // landed before this barrier; first read by S3(kk+1) (own column)
         if (kk + 4 < N + 2) load_plane(kk + 4);
         if (kk + 1 < N) stage_b(kk + 1);
         commit();
@@ -495,6 +534,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
         for (int v = 0; v < NV; v++) fzlo[v] = fzhi[v];
     }
+    if (!ok) flag_nonphysical(sc);
 }
 
 // ---------------------------------------------------------------- KD
@@ -902,7 +942,7 @@ struct RankPlan {
 // KB+KC fused (3-D 16^3 leaves, face-centric schemes): no face-flux array
 bool leaf_fused(const AmrGeo& g) {
     return g.ndim == 3 && g.nb[0] == spark::kLeafN && g.nb[1] == spark::kLeafN && g.nb[2] == spark::kLeafN &&
-           (g.recon == 0 || g.recon == 1 || g.recon == 3);
+           (g.recon == 0 || g.recon == 1 || g.recon == 3) && g.ng == spark::kLeafNG;
 }
 
 // per-leaf offsets of a guard list ordered by leaf (dst = leaf * np + ...)
@@ -1068,16 +1108,20 @@ void launched(cudaError_t e, const char* what) {
 }
 
 // padded tiles of state u: interior + face guards; primitives (to_prim) or conserved
-void amr_fill(spark_amr* a, const double* u, double* w, int to_prim) {
+// interior = 0: guards only (the fused leaf kernel reads the interior from U)
+void amr_fill(spark_amr* a, const double* u, double* w, int to_prim, int interior = 1) {
     const AmrGeo& g = a->rp.g;
     if (g.nleaf == 0) return;
     const unsigned nb = (unsigned)g.nleaf;
     if (g.ndim == 1)
-        spark::amr_fill_leaf_kernel<3><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim, a->sc);
+        spark::amr_fill_leaf_kernel<3><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim,
+                                                                  interior, a->sc);
     else if (g.ndim == 2)
-        spark::amr_fill_leaf_kernel<4><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim, a->sc);
+        spark::amr_fill_leaf_kernel<4><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim,
+                                                                  interior, a->sc);
     else
-        spark::amr_fill_leaf_kernel<5><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim, a->sc);
+        spark::amr_fill_leaf_kernel<5><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim,
+                                                                  interior, a->sc);
     launched(cudaGetLastError(), "amr fill");
 }
 
@@ -1095,7 +1139,8 @@ void faces_d(spark_amr* a, double bco) {
 template <int RECON, int RS>
 void leaf_t(spark_amr* a, const double* prev, const double* un, double sa, double sb, double* out) {
     const AmrGeo& g = a->rp.g;
-    const size_t smem = sizeof(double) * ((size_t)spark::kLeafSlots * g.nv * g.pn[0] * g.pn[1] +
+    const size_t smem = sizeof(double) * ((size_t)spark::kLeafSlots * g.nv * (spark::kLeafN + 2 * spark::kLeafNG) *
+                                              (spark::kLeafN + 2 * spark::kLeafNG) +
                                           2 * (size_t)g.nv * spark::kLeafN +
                                           2 * (size_t)g.nv * (spark::kLeafN + 1) * spark::kLeafN +
                                           2 * 4 * (size_t)g.nv * spark::kLeafN);
@@ -1114,7 +1159,7 @@ void leaf_r(spark_amr* a, int rs, const double* prev, const double* un, double s
 void amr_stage(spark_amr* a, const double* prev, const double* un, double sa, double sb, double* out) {
     const AmrGeo& g = a->rp.g;
     if (g.nleaf == 0) return;
-    amr_fill(a, prev, a->W, 1);
+    amr_fill(a, prev, a->W, 1, leaf_fused(g) ? 0 : 1);
     if (leaf_fused(g)) {
         const int rs = a->plan.c.riemann;
         if (g.recon == 0) leaf_r<0>(a, rs, prev, un, sa, sb, out);
