@@ -88,15 +88,17 @@ __device__ __forceinline__ double guard_value(const AmrGeo& g, const double* __r
            0.125;
 }
 
-// KA in one launch, one CTA per leaf: its interior cells, then its guard
-// entries (the map lists them leaf by leaf; goff[leaf] is the first).  The
-// guard sources are neighbour leaves' interiors, read while they are still in
-// L2 from the neighbouring CTAs' interior pass (the leaf order follows the
-// block grid).
+// KA in one launch, one CTA per leaf: its interior cells, the faces whose
+// guards are a plain copy of one same-level leaf of this rank (sface[leaf*6 +
+// face slot] = that leaf, found by the host from the guard map: contiguous
+// rows, no per-cell map entry), then the remaining guard entries (coarse-fine
+// faces, physical boundaries, other ranks; the map lists them leaf by leaf,
+// goff[leaf] is the first).  Same values as the per-entry map.
 template <int NV>
 __global__ void __launch_bounds__(256) amr_fill_leaf_kernel(const AmrGeo g, const double* __restrict__ u,
                                                             const GuardE* __restrict__ ge,
                                                             const long long* __restrict__ goff,
+                                                            const long long* __restrict__ sface,
                                                             const double* __restrict__ grecv, double* __restrict__ w,
                                                             int to_prim, int interior, DevScalars* sc) {
     const long long vs = g.nleaf * g.nc, vp = g.nleaf * g.np;
@@ -114,6 +116,31 @@ __global__ void __launch_bounds__(256) amr_fill_leaf_kernel(const AmrGeo g, cons
         if (to_prim) ok &= cons_to_prim<NV>(uu, ww, g.gamma - 1.0);
 #pragma unroll
         for (int v = 0; v < NV; v++) w[v * vp + p] = to_prim ? ww[v] : uu[v];
+    }
+    for (int f = 0; f < 2 * g.ndim; f++) {  // same-level faces: the neighbour's ng layers next to the face
+        const long long src_leaf = sface[leaf * 6 + f];
+        if (src_leaf < 0) continue;  // CTA-uniform
+        const int d = f >> 1, hi = f & 1;
+        const int a = d == 0 ? 1 : 0, b = d == 2 ? 1 : 2;  // the other two dims, x first when it is one
+        const int na = g.nb[a], n = g.ng * na * g.nb[b];
+        for (int m = threadIdx.x; m < n; m += blockDim.x) {
+            int t, ia, ib;  // layer, coordinates along a and b (the fastest index runs along x)
+            if (d == 0) { t = m % g.ng; ia = (m / g.ng) % na; ib = m / (g.ng * na); }
+            else { ia = m % na; t = (m / na) % g.ng; ib = m / (na * g.ng); }
+            int c[3], q[3];
+            c[a] = q[a] = ia;
+            c[b] = q[b] = ib;
+            c[d] = hi ? g.nb[d] + t : t - g.ng;    // guard cell of this leaf
+            q[d] = hi ? t : g.nb[d] - g.ng + t;    // the neighbour's cell
+            const long long dst = leaf * g.np + ((long long)(c[2] + gz) * g.pn[1] + (c[1] + gy)) * g.pn[0] + (c[0] + gx);
+            const long long src = src_leaf * g.nc + ((long long)q[2] * g.nb[1] + q[1]) * g.nb[0] + q[0];
+            double uu[NV], ww[NV];
+#pragma unroll
+            for (int v = 0; v < NV; v++) uu[v] = u[v * vs + src];
+            if (to_prim) ok &= cons_to_prim<NV>(uu, ww, g.gamma - 1.0);
+#pragma unroll
+            for (int v = 0; v < NV; v++) w[v * vp + dst] = to_prim ? ww[v] : uu[v];
+        }
     }
     const long long e1 = goff[leaf + 1];
 #pragma unroll 4
@@ -945,6 +972,66 @@ bool leaf_fused(const AmrGeo& g) {
            (g.recon == 0 || g.recon == 1 || g.recon == 3) && g.ng == spark::kLeafNG;
 }
 
+// Faces whose ng guard layers are a plain copy (kind 1, no reflect flip) of
+// the adjacent layers of ONE leaf of this rank: sface[leaf * 6 + slot] = that
+// leaf (else -1); the map keeps only the other entries.  Found by checking
+// every entry of the face against the copy pattern, so anything else (a
+// coarse-fine face, a boundary image, another rank's value) stays in the map.
+void compress_faces(const AmrGeo& g, std::vector<GuardE>& gs, std::vector<long long>& sface) {
+    const long long nl = g.nleaf;
+    sface.assign(nl * 6, -1);
+    std::vector<long long> cnt(nl * 6, 0), src(nl * 6, -1);
+    std::vector<char> bad(nl * 6, 0);
+    const int gl[3] = {g.ng, g.ndim >= 2 ? g.ng : 0, g.ndim >= 3 ? g.ng : 0};
+    auto slot_of = [&](const GuardE& e, int* c) {
+        long long p = e.dst % g.np;
+        c[0] = (int)(p % g.pn[0]) - gl[0];
+        c[1] = (int)((p / g.pn[0]) % g.pn[1]) - gl[1];
+        c[2] = (int)(p / ((long long)g.pn[0] * g.pn[1])) - gl[2];
+        int slot = -1, outside = 0;
+        for (int d = 0; d < 3; d++)
+            if (c[d] < 0 || c[d] >= g.nb[d]) {
+                slot = 2 * d + (c[d] >= g.nb[d] ? 1 : 0);
+                outside++;
+            }
+        return outside == 1 ? slot : -1;
+    };
+    for (const GuardE& e : gs) {
+        int c[3];
+        const int slot = slot_of(e, c);
+        if (slot < 0) continue;
+        const long long k = (e.dst / g.np) * 6 + slot;
+        cnt[k]++;
+        const int d = slot >> 1;
+        int q[3] = {c[0], c[1], c[2]};
+        q[d] += (slot & 1) ? -g.nb[d] : g.nb[d];
+        const long long want = ((long long)q[2] * g.nb[1] + q[1]) * g.nb[0] + q[0];
+        if (e.kind != 1 || e.src % g.nc != want) {
+            bad[k] = 1;
+            continue;
+        }
+        const long long sl = e.src / g.nc;
+        if (src[k] < 0) src[k] = sl;
+        else if (src[k] != sl) bad[k] = 1;
+    }
+    for (long long k = 0; k < nl * 6; k++) {
+        const int d = (int)(k % 6) >> 1;
+        if (d >= g.ndim || bad[k] || src[k] < 0) continue;
+        long long full = g.ng;
+        for (int e = 0; e < 3; e++)
+            if (e != d) full *= g.nb[e];
+        if (cnt[k] == full) sface[k] = src[k];
+    }
+    std::vector<GuardE> rest;
+    rest.reserve(gs.size());
+    for (const GuardE& e : gs) {
+        int c[3];
+        const int slot = slot_of(e, c);
+        if (slot < 0 || sface[(e.dst / g.np) * 6 + slot] < 0) rest.push_back(e);
+    }
+    gs.swap(rest);
+}
+
 // per-leaf offsets of a guard list ordered by leaf (dst = leaf * np + ...)
 std::vector<long long> guard_offsets(const std::vector<GuardE>& gs, long long nleaf, long long np) {
     std::vector<long long> off(nleaf + 1, 0);
@@ -1050,6 +1137,7 @@ size_t rank_bytes(const RankPlan& p) {
     b += al(sizeof(double) * g.nv * g.nleaf * g.np);            // padded tiles
     if (!leaf_fused(g)) b += al(sizeof(double) * g.nv * g.nleaf * g.NF);  // face fluxes (unfused KB/KC)
     b += al(sizeof(long long) * (g.nleaf + 1));                 // guard offsets per leaf
+    b += al(sizeof(long long) * 6 * std::max(1LL, g.nleaf));    // same-level face sources
     b += al(sizeof(double) * g.nv * g.nleaf * 6 * g.mf);        // fluxBuff
     b += al(sizeof(GuardE) * std::max<size_t>(1, p.guards.size()));
     for (int d = 0; d < 3; d++) b += al(sizeof(CorrE) * std::max<size_t>(1, p.corr[d].size()));
@@ -1079,7 +1167,8 @@ struct spark_amr {
     CorrE* corr[3] = {};
     GuardE* gitems = nullptr;
     long long* fitems = nullptr;
-    long long* goff = nullptr;  // first guard entry of each leaf
+    long long* goff = nullptr;   // first guard entry of each leaf
+    long long* sface = nullptr;  // same-level source leaf of each face slot (-1: map entries)
     double *gsend = nullptr, *grecv = nullptr, *fsend = nullptr, *frecv = nullptr;
     int n_idx = 0;
     bool have_state = false;
@@ -1114,13 +1203,13 @@ void amr_fill(spark_amr* a, const double* u, double* w, int to_prim, int interio
     if (g.nleaf == 0) return;
     const unsigned nb = (unsigned)g.nleaf;
     if (g.ndim == 1)
-        spark::amr_fill_leaf_kernel<3><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim,
+        spark::amr_fill_leaf_kernel<3><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->sface, a->grecv, w, to_prim,
                                                                   interior, a->sc);
     else if (g.ndim == 2)
-        spark::amr_fill_leaf_kernel<4><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim,
+        spark::amr_fill_leaf_kernel<4><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->sface, a->grecv, w, to_prim,
                                                                   interior, a->sc);
     else
-        spark::amr_fill_leaf_kernel<5><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->grecv, w, to_prim,
+        spark::amr_fill_leaf_kernel<5><<<nb, 256, 0, a->stream>>>(g, u, a->guards, a->goff, a->sface, a->grecv, w, to_prim,
                                                                   interior, a->sc);
     launched(cudaGetLastError(), "amr fill");
 }
@@ -1268,6 +1357,7 @@ void carve_member(spark_amr* a, void* arena, size_t arena_bytes) {
     a->W = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * g.np));
     if (!leaf_fused(g)) a->F = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * g.NF));
     a->goff = reinterpret_cast<long long*>(take(sizeof(long long) * (g.nleaf + 1)));
+    a->sface = reinterpret_cast<long long*>(take(sizeof(long long) * 6 * std::max(1LL, g.nleaf)));
     a->B = reinterpret_cast<double*>(take(sizeof(double) * g.nv * g.nleaf * 6 * g.mf));
     a->guards = reinterpret_cast<GuardE*>(take(sizeof(GuardE) * std::max<size_t>(1, rp.guards.size())));
     for (int d = 0; d < 3; d++)
@@ -1282,9 +1372,13 @@ void carve_member(spark_amr* a, void* arena, size_t arena_bytes) {
     auto up = [&](void* dst, const void* src, size_t bytes) {
         if (bytes) ACU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, a->stream));
     };
-    up(a->guards, rp.guards.data(), sizeof(GuardE) * rp.guards.size());
-    const std::vector<long long> goff = guard_offsets(rp.guards, g.nleaf, g.np);
+    std::vector<GuardE> gmap = rp.guards;  // minus the faces copied as whole slabs
+    std::vector<long long> sface;
+    compress_faces(g, gmap, sface);
+    up(a->guards, gmap.data(), sizeof(GuardE) * gmap.size());
+    const std::vector<long long> goff = guard_offsets(gmap, g.nleaf, g.np);
     up(a->goff, goff.data(), sizeof(long long) * goff.size());
+    up(a->sface, sface.data(), sizeof(long long) * sface.size());
     for (int d = 0; d < 3; d++) up(a->corr[d], rp.corr[d].data(), sizeof(CorrE) * rp.corr[d].size());
     up(a->gitems, rp.gsend.data(), sizeof(GuardE) * ngs);
     up(a->fitems, rp.fsend.data(), sizeof(long long) * nfs);
