@@ -496,10 +496,16 @@ __global__ void __launch_bounds__(256, 2)
     __syncthreads();  // plane -2 read by every thread
     load_plane(3);
     commit();
-    // (an L2 prefetch of the S4 operands one or two planes ahead measured
-    // slower: 6.42 -> 5.98 G zone-updates/s)
+    // (an L2 prefetch of both S4 operands one or two planes ahead measured
+    // slower: 6.42 -> 5.98 G zone-updates/s; U^(s-1) of the plane is in L2
+    // from the plane copy anyway)
     for (int kk = 0; kk < N; kk++) {
         const int pb = kk & 1;
+        if (a != 0.0) {  // U^n of this plane into L2 while S3 runs (as KB1): 7.48 -> 7.78 G (a plane earlier: same)
+            const long long c = leaf * g.nc + ((long long)kk * N + tj) * N + ti;
+#pragma unroll
+            for (int v = 0; v < NV; v++) asm volatile("prefetch.global.L2 [%0];" ::"l"(un + v * vs + c));
+        }
         double* const XK = XA + pb * NV * N;
         double* const YK = YA + pb * NV * (N + 1) * N;
         const double* const cur = plane(kk);
