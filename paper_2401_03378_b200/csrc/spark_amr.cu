@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) amr_fill_leaf_kernel(const AmrGeo g, cons
 #pragma unroll
         for (int v = 0; v < NV; v++) w[v * vp + p] = to_prim ? ww[v] : uu[v];
     }
-    for (int f = 0; f < 2 * g.ndim; f++) {  // same-level faces: the neighbour's ng layers next to the face
+    for (int f = 0; interior && f < 2 * g.ndim; f++) {  // same-level faces (the fused leaf kernel copies them itself)
         const long long src_leaf = sface[leaf * 6 + f];
         if (src_leaf < 0) continue;  // CTA-uniform
         const int d = f >> 1, hi = f & 1;
@@ -328,8 +328,8 @@ __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
 template <int RECON, int RS>
 __global__ void __launch_bounds__(256, 2)
     amr_leaf_kernel(const AmrGeo g, const double* __restrict__ w, const double* __restrict__ uprev,
-                    const double* __restrict__ un, double* __restrict__ uout, double* __restrict__ B, double a,
-                    double bco, DevScalars* __restrict__ sc) {
+                    const double* __restrict__ un, double* __restrict__ uout, double* __restrict__ B,
+                    const long long* __restrict__ sface, double a, double bco, DevScalars* __restrict__ sc) {
     constexpr int NV = 5, N = kLeafN, NS = kLeafSlots;
     extern __shared__ double smem[];
     constexpr int gd = kLeafNG, pn0 = N + 2 * gd;  // the tile's guard depth (leaf_fused)
@@ -351,51 +351,79 @@ __global__ void __launch_bounds__(256, 2)
     const double* const Wl = w + leaf * g.np;
     auto plane = [&](int z) { return ring + ((z + 2 * NS) % NS) * NV * PL; };
     const int own = (tj + gd) * pn0 + ti + gd;  // this column's cell in a padded plane
-    // padded plane z (all variables) into its slot: a guard plane (z < 0 or
-    // z >= N) whole from W; an interior plane's N x N interior as CONSERVED
-    // values straight from U^(s-1) (converted in place by each column's
-    // thread, convert() below; KA then writes no interior) and its guard
-    // frame from W.  16-byte copies (gd even: every row piece is aligned).
+    // padded plane z (all variables) into its slot, 16-byte copies.  Interior
+    // plane: its N x N interior as CONSERVED values straight from U^(s-1);
+    // the guard frame face by face: from the same-level neighbour's U^(s-1)
+    // (conserved) where sface names one, else from W (primitive, filled by
+    // KA).  Guard plane (z < 0 or z >= N): only its centre is ever read (the
+    // own column's z stencil): from the neighbour below / above, else W.
+    // The conserved cells are converted in place by convert() a plane later.
+    long long sf[6];
+#pragma unroll
+    for (int f = 0; f < 6; f++) sf[f] = sface[leaf * 6 + f];
     auto load_plane = [&](int z) {
         double* dst = plane(z);
-        const double* src = Wl + (long long)(z + gd) * PL;
+        const double* wz = Wl + (long long)(z + gd) * PL;  // W plane z
         if (z < 0 || z >= N) {
-            const int half = PL / 2;
-            for (int e = tid; e < NV * half; e += blockDim.x) {
-                const int v = e / half, c = e - v * half;
-                cp_async16(dst + v * PL + 2 * c, src + v * vp + 2 * c);
+            const long long L = sf[z < 0 ? 4 : 5];
+            const double* uz = uprev + L * g.nc + (long long)(z < 0 ? z + N : z - N) * N * N;
+            for (int e = tid; e < NV * (N * N / 2); e += blockDim.x) {
+                const int v = e / (N * N / 2), c = e - v * (N * N / 2);
+                const int r = c / (N / 2), x = 2 * (c - r * (N / 2));
+                const int pp = (r + gd) * pn0 + gd + x;
+                cp_async16(dst + v * PL + pp, L >= 0 ? uz + v * vs + r * N + x : wz + v * vp + pp);
             }
             return;
         }
-        const int nint = N * N / 2, nrow = gd * pn0, per = nint + nrow + N * gd;  // 16-byte pieces per variable
-        const double* uz = uprev + leaf * g.nc + (long long)z * N * N;
+        constexpr int nint = N * N / 2, per = nint + 4 * N;  // pieces per variable: interior + 4 frame sides
+        const long long zo = (long long)z * N * N;
         for (int e = tid; e < NV * per; e += blockDim.x) {
             const int v = e / per;
             int c = e - v * per;
             if (c < nint) {  // interior row r, pieces of 2
                 const int r = c / (N / 2), x = 2 * (c - r * (N / 2));
-                cp_async16(dst + v * PL + (r + gd) * pn0 + gd + x, uz + v * vs + r * N + x);
-            } else if ((c -= nint) < nrow) {  // the gd rows below and above the interior
-                const int rr = c / (pn0 / 2), x = 2 * (c - rr * (pn0 / 2));
-                const int y = rr < gd ? rr : rr + N;  // padded row
-                cp_async16(dst + v * PL + y * pn0 + x, src + v * vp + y * pn0 + x);
-            } else {  // left / right guard columns of the interior rows
-                c -= nrow;
-                const int r = c / gd, k = c - r * gd;  // k < gd / 2: left, else right
-                const int x = k < gd / 2 ? 2 * k : gd + N + 2 * (k - gd / 2);
-                cp_async16(dst + v * PL + (r + gd) * pn0 + x, src + v * vp + (r + gd) * pn0 + x);
+                cp_async16(dst + v * PL + (r + gd) * pn0 + gd + x, uprev + v * vs + leaf * g.nc + zo + r * N + x);
+                continue;
             }
+            c -= nint;
+            const int f = c / N, k = c - f * N;  // frame side f (x-, x+, y-, y+), piece k
+            int pp, sc;                           // padded position, neighbour cell (in its plane)
+            if (f < 2) {  // 2 cells of row k
+                pp = (k + gd) * pn0 + (f ? gd + N : 0);
+                sc = k * N + (f ? 0 : N - gd);
+            } else {      // 2 cells of column pair 2 (k % 8) in row k / 8 of the frame
+                const int rr = k / (N / 2), x = 2 * (k - rr * (N / 2));
+                pp = (f == 2 ? rr : gd + N + rr) * pn0 + gd + x;
+                sc = (f == 2 ? N - gd + rr : rr) * N + x;
+            }
+            const long long L = sf[f];
+            cp_async16(dst + v * PL + pp, L >= 0 ? uprev + v * vs + L * g.nc + zo + sc : wz + v * vp + pp);
         }
     };
     bool ok = true;
-    auto convert = [&](int z) {  // this column's cell of interior plane z: conserved -> primitive
-        double* c = plane(z) + own;
+    auto cvt = [&](double* c) {  // one cell of a slot: conserved -> primitive in place
         double u[NV], wv[NV];
 #pragma unroll
         for (int v = 0; v < NV; v++) u[v] = c[v * PL];
         ok &= cons_to_prim<NV>(u, wv, g.gamma - 1.0);
 #pragma unroll
         for (int v = 0; v < NV; v++) c[v * PL] = wv[v];
+    };
+    // the conserved cells of plane z: this column's centre cell (interior
+    // planes; guard planes copied from a neighbour) and, on threads 0-127,
+    // one frame cell of a side copied from a neighbour
+    auto convert = [&](int z) {
+        const bool inner = z >= 0 && z < N;
+        if (inner || sf[z < 0 ? 4 : 5] >= 0) cvt(plane(z) + own);
+        if (inner && tid < 4 * 2 * N) {
+            const int f = tid / (2 * N), k = tid - f * 2 * N;
+            if (sf[f] >= 0) {
+                int pp;
+                if (f < 2) pp = (k / gd + gd) * pn0 + (f ? gd + N : 0) + k % gd;
+                else pp = (f == 2 ? k / N : gd + N + k / N) * pn0 + gd + k % N;
+                cvt(plane(z) + pp);
+            }
+        }
     };
     auto stage_b = [&](int z) {  // fluxBuff of plane z's x / y leaf faces -> BS[z & 1]
         double* dst = BS + (z & 1) * 4 * NV * N;
@@ -485,7 +513,7 @@ __global__ void __launch_bounds__(256, 2)
     commit();
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
-    for (int z = 0; z <= 2; z++) convert(z);  // own cells: read by this thread first, by others after the next barrier
+    for (int z = -2; z <= 2; z++) convert(z);  // read by this thread first, by others after the next barrier
     double fzlo[NV], fzhi[NV];
     {
         const double* q[4];
@@ -542,7 +570,7 @@ __global__ void __launch_bounds__(256, 2)
         // ---------------------------------------------------------- S4
         // plane kk+4 into plane kk-1's slot (read by S3 of plane kk only) and the
         // fluxBuff values of plane kk+1 (BS[(kk+1) & 1], last read in S4(kk-1))
-        if (kk + 3 < N) convert(kk + 3);  // landed before this barrier; first read by S3(kk+1) (own column)
+        if (kk + 3 < N + gd) convert(kk + 3);  // landed before this barrier; first read by S3(kk+1) (own column)
         if (kk + 4 < N + 2) load_plane(kk + 4);
         if (kk + 1 < N) stage_b(kk + 1);
         commit();
@@ -1203,7 +1231,8 @@ void launched(cudaError_t e, const char* what) {
 }
 
 // padded tiles of state u: interior + face guards; primitives (to_prim) or conserved
-// interior = 0: guards only (the fused leaf kernel reads the interior from U)
+// interior = 0: the map entries only (the fused leaf kernel reads the
+// interior and the same-level faces straight from U)
 void amr_fill(spark_amr* a, const double* u, double* w, int to_prim, int interior = 1) {
     const AmrGeo& g = a->rp.g;
     if (g.nleaf == 0) return;
@@ -1241,7 +1270,7 @@ void leaf_t(spark_amr* a, const double* prev, const double* un, double sa, doubl
                                           2 * 4 * (size_t)g.nv * spark::kLeafN);
     auto k = spark::amr_leaf_kernel<RECON, RS>;
     launched(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "amr leaf smem");
-    k<<<(unsigned)g.nleaf, 256, smem, a->stream>>>(g, a->W, prev, un, out, a->B, sa, sb, a->sc);
+    k<<<(unsigned)g.nleaf, 256, smem, a->stream>>>(g, a->W, prev, un, out, a->B, a->sface, sa, sb, a->sc);
 }
 
 template <int RECON>
