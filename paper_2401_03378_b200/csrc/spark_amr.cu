@@ -507,7 +507,13 @@ __global__ void __launch_bounds__(256, 2)
     };
 
     // prologue: planes -2 .. 2, the z face below plane 0, then plane 3 into
-    // plane -2's slot
+    // plane -2's slot; the fluxBuff values of the two z leaf faces of this
+    // column (read-modify-written in the prologue and after the last plane)
+    // requested into L2 first
+#pragma unroll
+    for (int v = 0; v < NV; v++)
+        for (int slot = 4; slot < 6; slot++)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(B + v * bvs + (leaf * 6 + slot) * g.mf + tj * N + ti));
     for (int z = -2; z <= 2; z++) load_plane(z);
     stage_b(0);
     commit();
