@@ -127,7 +127,24 @@ def draw_amr(i):
     return p, tuple(rlo), tuple(rhi), int(g.integers(1, 4))
 
 
-AMR = [draw_amr(i) for i in range(40)]
+def draw_amr16(i):
+    """16^3 leaves (the fused leaf kernel's shape) with random boxes, boundaries,
+    face-centric scheme and rank count."""
+    g = np.random.Generator(np.random.PCG64(7000 + i))
+    nblk = tuple(int(g.integers(2, 4)) for _ in range(3))
+    bc = tuple((0, 0) if g.random() < 0.35 else (int(g.integers(1, 3)), int(g.integers(1, 3))) for _ in range(3))
+    recon = int(g.choice([0, 1, 3]))
+    riemann = int(g.integers(0, 3 if recon else 2))
+    p = si.Problem(f"a16_{i}", 3, (16, 16, 16), nblk, 2, recon, riemann, int(g.integers(2, 4)), 0.3, bc=bc,
+                   shock_thresh=float(g.uniform(0.2, 1.0)) if riemann == 2 else 0.0)
+    rlo, rhi = [0, 0, 0], [1, 1, 1]
+    for d in range(3):  # a non-empty box: the coarse-fine faces are the point
+        a = int(g.integers(0, nblk[d]))
+        rlo[d], rhi[d] = a, int(g.integers(a + 1, nblk[d] + 1))
+    return p, tuple(rlo), tuple(rhi), int(g.integers(1, 4))
+
+
+AMR = [draw_amr(i) for i in range(40)] + [draw_amr16(i) for i in range(8)]
 
 
 @pytest.mark.parametrize("case", AMR, ids=ids)
