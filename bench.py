@@ -381,6 +381,7 @@ def run_reference(args, rank, world):
     import oracle
 
     oracle.build()
+    oracle.set_threads(0)  # every host core, also under torchrun (which sets OMP_NUM_THREADS=1)
     q = p.with_(nblk=tuple(min(4, p.nblk[d]) for d in range(3)))
     U = oracle.prim_to_cons(q.ndim, q.gamma, si.initial_primitive(q))
     for _ in range(args.warmup):
