@@ -411,7 +411,7 @@ std::pair<cudaEvent_t, cudaEvent_t> prof_events(spark_ctx* c) {
 // (default the context's); timed: bracket the launch with profiling events
 void stage_launch(spark_ctx* c, const double* prev, const double* un, double a, double b, double* out,
                   bool last, const double* dt_ptr, double dt_value, bool honor_active, int part = 0,
-                  cudaStream_t st = nullptr, bool timed = true) {
+                  cudaStream_t st = nullptr, bool timed = true, int blk0 = 0, int nblk = 0) {
     if (!st) st = c->stream;
     spark::StageArgs A{};
     A.g = c->plan.geo;
@@ -428,6 +428,8 @@ void stage_launch(spark_ctx* c, const double* prev, const double* un, double a, 
     A.last = last ? 1 : 0;
     A.honor_active = honor_active ? 1 : 0;
     A.part = part;
+    A.blk0 = blk0;
+    A.nblk = nblk;
     const bool ev = c->prof && timed;
     std::pair<cudaEvent_t, cudaEvent_t> e{};
     if (ev) {
@@ -1127,14 +1129,18 @@ spark_status spark_step_group(spark_ctx* const* ctxs, int32_t n, double dt, doub
     });
 }
 
-// One step with host buffers, the copies pipelined with the device work:
-// the state is moved in nchunks block ranges; chunk j of the upload waits only
-// for chunk j of the previous call's download (full-duplex PCIe: this call's
-// H2D overlaps the previous call's D2H), its relayout runs as soon as it has
-// arrived; the download of chunk j starts when its relayout out of the new
-// U^n is done.  Staging: canonical copies go through the two state buffers
-// that are dead at that point (in: the stage-1 output buffer before stage 1;
-// out: the buffer after U^(n+1)), chunk by chunk, so no extra memory.
+// One step with host buffers, the copies pipelined with the device work.
+// The state moves in nchunks block ranges as pitched copies straight between
+// the canonical host layout [v][b][cell] and the block-interleaved device
+// layout [b][v][cell] (one 2-D copy per range and variable: no staging
+// buffer, no relayout kernel).  Upload chunk j waits only for chunk j of the
+// previous call's download (U_in may be the previous U_out; full-duplex
+// PCIe: this call's H2D overlaps the previous call's D2H).  After the CFL
+// minimum of the whole uploaded U^n (dt is global) and the first S-1 stages,
+// the last stage runs range by range on a single-rank context, and range j's
+// download starts as soon as its blocks are written, under the remaining
+// ranges' compute; a multi-rank context runs the last stage whole (its
+// interior / rank-boundary split) and then downloads range by range.
 spark_status spark_step_host(spark_ctx* ctx, const double* U_in, double* U_out, double dt, double t_end,
                              int32_t nchunks) {
     if (!ctx || !U_in || !U_out || nchunks < 1) return SPARK_ERR_ARG;
@@ -1161,24 +1167,29 @@ spark_status spark_step_host(spark_ctx* ctx, const double* U_in, double* U_out, 
             *b0 = nblk * j / m;
             *b1 = nblk * (j + 1) / m;
         };
-        auto segs = [&](cudaStream_t st, const double* src, double* dst, long long b0, long long b1,
-                        cudaMemcpyKind kind) {
+        // blocks [b0, b1) of variable v: host U[v][b][cell] <-> device D[b][v][cell]
+        const size_t cell_bytes = sizeof(double) * (size_t)g.cpb;
+        auto copy = [&](cudaStream_t st, const double* host_src, double* dev_dst, const double* dev_src,
+                        double* host_dst, long long b0, long long b1) {
             for (int v = 0; v < g.nvar; v++) {
-                const size_t off = (size_t)v * g.ncell + (size_t)b0 * g.cpb;
-                CU(cudaMemcpyAsync(dst + off, src + off, sizeof(double) * (size_t)(b1 - b0) * g.cpb, kind, st));
+                const size_t h = (size_t)v * g.ncell + (size_t)b0 * g.cpb, d = (size_t)b0 * g.bs + (size_t)v * g.vs;
+                if (host_src)
+                    CU(cudaMemcpy2DAsync(dev_dst + d, sizeof(double) * g.bs, host_src + h, cell_bytes, cell_bytes,
+                                         (size_t)(b1 - b0), cudaMemcpyHostToDevice, st));
+                else
+                    CU(cudaMemcpy2DAsync(host_dst + h, cell_bytes, dev_src + d, sizeof(double) * g.bs, cell_bytes,
+                                         (size_t)(b1 - b0), cudaMemcpyDeviceToHost, st));
             }
         };
         const int n = ctx->n_idx;
-        double* Sin = ctx->U[(n + 1) % 3];
-        // ---- in: H2D chunk j (after the previous call's D2H of chunk j) -> relayout into U^n
+        // ---- in: H2D chunk j (after the previous call's D2H of chunk j) -> U^n
         for (int j = 0; j < m; j++) {
             long long b0, b1;
             range(j, &b0, &b1);
             CU(cudaStreamWaitEvent(ctx->h2d, ctx->ev_d2h[j], 0));
-            segs(ctx->h2d, U_in, Sin, b0, b1, cudaMemcpyHostToDevice);
+            copy(ctx->h2d, U_in, ctx->U[n], nullptr, nullptr, b0, b1);
             CU(cudaEventRecord(ctx->ev_h2d[j], ctx->h2d));
             CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_h2d[j], 0));
-            launched(ctx, spark::launch_relayout_range(g, Sin, ctx->U[n], 1, b0, b1, ctx->stream), "relayout");
         }
         // ---- the step: CFL minimum of the uploaded U^n (global), then the stages
         launched(ctx, spark::launch_acc_reset(ctx->sc, ctx->stream), "acc reset");
@@ -1186,18 +1197,41 @@ spark_status spark_step_host(spark_ctx* ctx, const double* U_in, double* U_out, 
         allreduce_acc(ctx);
         ctx->have_state = true;
         launched(ctx, spark::launch_step_begin(ctx->sc, dt, t_end, ctx->cfg.cfl, ctx->stream), "step begin");
-        do_step(ctx, dt);
-        // ---- out: relayout chunk j of U^(n+1) -> D2H chunk j
-        const int nn = ctx->n_idx;
-        double* Sout = ctx->U[(nn + 1) % 3];
-        for (int j = 0; j < m; j++) {
+        auto download = [&](int j, const double* src) {  // range j of src, after the compute stream's work so far
             long long b0, b1;
             range(j, &b0, &b1);
-            launched(ctx, spark::launch_relayout_range(g, ctx->U[nn], Sout, 0, b0, b1, ctx->stream), "relayout");
             CU(cudaEventRecord(ctx->ev_out[j], ctx->stream));
             CU(cudaStreamWaitEvent(ctx->d2h, ctx->ev_out[j], 0));
-            segs(ctx->d2h, Sout, U_out, b0, b1, cudaMemcpyDeviceToHost);
+            copy(ctx->d2h, nullptr, nullptr, src, U_out, b0, b1);
             CU(cudaEventRecord(ctx->ev_d2h[j], ctx->d2h));
+        };
+        if (ctx->comm) {
+            do_step(ctx, dt);
+            for (int j = 0; j < m; j++) download(j, ctx->U[ctx->n_idx]);
+        } else {
+            Nvtx step_range("spark step (host buffers)");
+            const int S = ctx->cfg.rk_stages;
+            int newn = n;
+            for (int s = 1; s <= S; s++) {
+                int pi, po;
+                newn = stage_buffers(S, n, s, &pi, &po);
+                double a, b;
+                rk_coeffs(S, s, &a, &b);
+                if (s < S) {
+                    stage_launch(ctx, ctx->U[pi], ctx->U[n], a, b, ctx->U[po], false, &ctx->sc->dt, dt, true);
+                    continue;
+                }
+                for (int j = 0; j < m; j++) {  // the last stage range by range, each range downloaded at once
+                    long long b0, b1;
+                    range(j, &b0, &b1);
+                    stage_launch(ctx, ctx->U[pi], ctx->U[n], a, b, ctx->U[po], true, &ctx->sc->dt, dt, true, 0,
+                                 nullptr, false, (int)b0, (int)(b1 - b0));
+                    if (j > 0) ctx->stage_launches--;  // the ranges of one stage count once
+                    download(j, ctx->U[po]);
+                }
+            }
+            allreduce_acc(ctx);
+            ctx->n_idx = newn;
         }
         // a later synchronisation of the context stream covers the downloads
         CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_d2h[m - 1], 0));

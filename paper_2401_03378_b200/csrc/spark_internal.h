@@ -69,6 +69,7 @@ struct StageArgs {
     int honor_active;             // 1: copy-through when sc->active == 0
     int part;                     // 0 all blocks; 1 blocks touching no exchanged rank face
                                   // ("interior", run while halos travel); 2 the others
+    int blk0, nblk;               // block range of the launch (nblk 0: all blocks)
 };
 
 // Telescoping through HBM tiles (spark_telescope_tile.cu): G = S*NGK guard

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, NDIM == 3 ? 2 : 3) stage_kernel(cons
     const int tid = threadIdx.x;
     const bool live = tid < P;
     const int ti = live ? tid % nb0 : 0, tj = live ? tid / nb0 : 0;
-    const int b = blockIdx.x;
+    const int b = A.blk0 + (int)blockIdx.x;  // a block range (spark_step_host's pipelined last stage)
     const int bx = b % g.bn[0], by = (b / g.bn[0]) % g.bn[1], bz = b / (g.bn[0] * g.bn[1]);
     const int cx0 = bx * nb0, cy0 = by * nb1, cz0 = bz * nb2;
     // block-interleaved state U[b][v][c]: with a compile-time block shape the
@@ -990,7 +990,7 @@ cudaError_t launch_t(const StageArgs& a, cudaStream_t s) {
     auto k = stage_kernel<NDIM, RECON, RS, NBX, NBY, NBZ>;
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
-    const long long nblk = (long long)a.g.bn[0] * a.g.bn[1] * a.g.bn[2];
+    const long long nblk = a.nblk > 0 ? a.nblk : (long long)a.g.bn[0] * a.g.bn[1] * a.g.bn[2];
     k<<<(unsigned)nblk, stage_block_threads(a.g, RECON), smem, s>>>(a);
     return cudaGetLastError();
 }
