@@ -32,7 +32,7 @@ cap() { tag=$1; kern=$2; skip=$3; cnt=$4; shift 4
 cap c4_plm stage_kernel 4 2 --steps 3 --warmup 3 $Q
 cap c4_weno stage_kernel 5 3 --config c4_sedov3d_weno --steps 3 --warmup 3 $Q
 cap c4_hybrid stage_kernel 4 2 --riemann hybrid --steps 3 --warmup 3 $Q
-cap c4_amr amr_face_kernel 6 1 --amr --steps 2 --warmup 3
+cap c4_amr amr_leaf_kernel 6 1 --amr --steps 2 --warmup 3
 cap c4_tel tt_face_kernel 6 1 --telescoping --steps 2 --warmup 3 $Q
 python tools/fp64_count.py $R/prof_c4_plm.ncu-rep stage_kernel 16777216 > $O/instmix_c4_plm.txt 2>&1
 python tools/fp64_count.py $R/prof_c4_weno.ncu-rep stage_kernel 16777216 > $O/instmix_c4_weno.txt 2>&1
