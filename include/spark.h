@@ -239,10 +239,12 @@ spark_status spark_run(spark_ctx* ctx, int64_t nsteps, double dt, double t_end);
  * pinned for asynchronous copies): upload U_in, step (dt, t_end as spark_step;
  * t and the step count continue — they are not reset as by spark_set_state),
  * download the new U^n to U_out (may alias U_in).  The transfers move nchunks
- * block ranges: chunk j of the upload waits only for chunk j of the previous
+ * block ranges, as pitched copies between the canonical host layout and the
+ * device pool: chunk j of the upload waits only for chunk j of the previous
  * call's download, so consecutive calls overlap their downloads with the next
- * uploads (full-duplex PCIe), and each chunk's relayout overlaps the remaining
- * copies.  Asynchronous: the host buffers must stay valid until the context
+ * uploads (full-duplex PCIe); on a single-rank context the last RK stage runs
+ * range by range and each range's download starts under the remaining
+ * ranges' compute.  Asynchronous: the host buffers must stay valid until the context
  * stream is synchronised (the stream waits for the last download).  Errors
  * surface at the next synchronising call. */
 spark_status spark_step_host(spark_ctx* ctx, const double* U_in, double* U_out, double dt, double t_end,
