@@ -436,7 +436,7 @@ def main():
     ap.add_argument("--amr", action="store_true",
                     help="NEXT N3: time the static two-level refinement (spark_amr_step) on the config's grid "
                          "with its central quarter of blocks per dimension refined (one GPU)")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
